@@ -1,0 +1,148 @@
+/*
+ * mmk.h — C ABI of the B200 (sm_100a) image path: preprocess -> encode -> pack/handoff.
+ *
+ * This is the drop-in boundary for the image path of a ModServe-style server.  The
+ * reference (arXiv 2502.00937, `lmmsim`, mounted read-only at /root/reference) models that
+ * path with three stand-ins that the functions below replace with real execution:
+ *
+ *   reference symbol (file:line)                                   replaced by
+ *   ------------------------------------------------------------   -----------------------------
+ *   core.tile_count / image_tokens      core.py:58-74              mmk_tile_plan   (K0, bit-exact)
+ *   Request.total_image_tokens/tiles    core.py:110-120            mmk_tile_plan   (int64 offsets)
+ *   LatencyProfile.preprocess_latency   profiles.py:128-134        mmk_preprocess  (K1)
+ *   LatencyProfile.encode_latency       profiles.py:136-145        mmk_gemm_bf16 / mmk_layernorm_f32
+ *                                                                  / mmk_attention_varlen_bf16 /
+ *                                                                  mmk_embed_* (K2-K8)
+ *   shard join + handoff                engine.py:730-752, :563-579 mmk_pack_* (K9) + NCCL P2P (K10,
+ *                                                                  host side, torch.distributed)
+ *
+ * Conventions (all functions):
+ *   - return int status: MMK_OK, MMK_ERR_ARG (-> SpecError), MMK_ERR_UNSUPPORTED
+ *     (-> ProfileError), MMK_ERR_CUDA (-> RuntimeError); mmk_last_error() has the message.
+ *   - every pointer is a DEVICE pointer unless noted; the caller owns all memory; nothing
+ *     here allocates device memory or synchronises; the stream is the last argument.
+ *   - stateless and re-entrant (per-thread error string), safe on distinct streams.
+ */
+#ifndef MMK_H_
+#define MMK_H_
+
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum mmk_status { MMK_OK = 0, MMK_ERR_ARG = 1, MMK_ERR_UNSUPPORTED = 2, MMK_ERR_CUDA = 3 };
+
+/* GEMM epilogues (mmk_gemm_bf16). */
+enum mmk_epilogue {
+  MMK_EPI_BF16 = 0,           /* out bf16 = acc + bias                              */
+  MMK_EPI_BF16_GELU = 1,      /* out bf16 = gelu_erf(acc + bias)     (Mllama FC1)   */
+  MMK_EPI_BF16_QUICKGELU = 2, /* out bf16 = quick_gelu(acc + bias)   (CLIP FC1)     */
+  MMK_EPI_F32 = 3,            /* out f32  = acc + bias               (patch embed)  */
+  MMK_EPI_RESID_F32 = 4       /* out f32 += gate * (acc + bias); aux bf16 = out     */
+};
+
+const char* mmk_version(void);
+const char* mmk_last_error(void);
+
+/*
+ * K0 — tile plan + ragged offsets.  Replaces core.tile_count (core.py:58-69),
+ * core.image_tokens (core.py:72-74) and Request.total_tiles / total_image_tokens
+ * (core.py:110-120) for n images at once, and adds the pixel geometry of each image.
+ *   in : w[n], h[n] (int32 pixels, >= 1), tile edge T, tokens/tile, cap, thumbnail flag
+ *   out: tiles[n]; tile_off[n+1], tok_off[n+1] (int64 exclusive prefix sums);
+ *        geom[n*4] = {rows, cols, resized_w, resized_h} of the tile canvas;
+ *        bad[1] (int32) = number of images with w<1 or h<1 (their tiles are 0).
+ * Single launch, one CTA, n <= 65536.
+ */
+int mmk_tile_plan(const int32_t* w, const int32_t* h, int32_t n, int32_t tile_px,
+                  int32_t tokens_per_tile, int32_t max_tiles, int32_t thumbnail, int32_t* tiles,
+                  int64_t* tile_off, int64_t* tok_off, int32_t* geom, int32_t* bad,
+                  cudaStream_t stream);
+
+/*
+ * K1 — fused uint8 HWC -> resize (bilinear, fp32) -> pad -> normalize -> tile -> patchify.
+ *   src       : concatenated uint8 RGB HWC images; src_off[n] byte offsets
+ *   w, h      : source dims; tile_off[n+1], geom[n*4] from mmk_tile_plan
+ *   mode      : 0 = canvas fit + zero pad (Mllama), 1 = shortest-side resize + centre crop (CLIP)
+ *   scale3[3], shift3[3]: normalisation out = (v * (1/255) - mean) * (1/std) as two fp32 ops:
+ *               out = v * scale3[c] + shift3[c] evaluated as round(round(v*s)+b)
+ *   patches   : bf16 [total_tiles * (T/p)^2, k_pad], patch vector order (c, py, px) like
+ *               nn.Conv2d weight flattening; columns [3*p*p, k_pad) are zero-filled.
+ */
+int mmk_preprocess(const uint8_t* src, const int64_t* src_off, const int32_t* w, const int32_t* h,
+                   const int64_t* tile_off, const int32_t* geom, int32_t n, int32_t total_tiles,
+                   int32_t tile_px, int32_t patch_px, int32_t k_pad, int32_t mode,
+                   int32_t thumbnail, const float* scale3, const float* shift3, void* patches,
+                   cudaStream_t stream);
+
+/*
+ * K2/K4/K6/K7/K8 — D[M,N] = A[M,K] . B[N,K]^T on tcgen05 tensor cores (bf16 in, fp32 acc),
+ * with the fused epilogue `epilogue` (enum mmk_epilogue).  lda/ldb/ldo/ld_aux in elements.
+ * bias: f32 [N] or NULL.  gate: residual scale (RESID_F32 only).  aux: optional bf16 copy of
+ * the updated residual (intermediate-layer capture for K9), RESID_F32 only.
+ */
+int mmk_gemm_bf16(const void* a, int64_t lda, const void* b, int64_t ldb, int32_t m, int32_t n,
+                  int32_t k, int32_t epilogue, const float* bias, void* out, int64_t ldo,
+                  float gate, void* aux, int64_t ld_aux, cudaStream_t stream);
+
+/*
+ * K3 — row LayerNorm: y_bf16 = LN(x_f32) * gamma + beta (+ optional per-tile additive term).
+ *   x f32 [rows, d]; y bf16 [rows, d] (or f32 when y_f32 != 0, may alias x).
+ *   tile_add (optional, f32 [n_tables, slots, d]) : y += tile_add[table[tile], slot[tile]]
+ *   where tile = row / rows_per_tile; tile_table/tile_slot int32 [n_tiles].
+ */
+int mmk_layernorm(const float* x, void* y, int32_t y_f32, int32_t rows, int32_t d,
+                  const float* gamma, const float* beta, float eps, const float* tile_add,
+                  const int32_t* tile_table, const int32_t* tile_slot, int32_t rows_per_tile,
+                  int32_t slots, cudaStream_t stream);
+
+/*
+ * K5 — non-causal variable-length multi-head self-attention (one sequence per image).
+ *   qkv bf16 [T, 3*H*hd] = [Q | K | V] (head h at column h*hd inside each block)
+ *   out bf16 [T, H*hd]; cu_seqlens int32 [n_seq+1]; hd in {64, 80}; scale = hd^-0.5 typically.
+ */
+int mmk_attention_varlen_bf16(const void* qkv, void* out, const int32_t* cu_seqlens, int32_t n_seq,
+                              int32_t max_seqlen, int32_t heads, int32_t head_dim, float scale,
+                              cudaStream_t stream);
+
+/*
+ * Embedding assembly (feeds K3 of layer 0): patch-embed output + class token + positional
+ * terms, then LayerNorm (`layernorm_pre`), written to the fp32 residual stream.
+ *   patch_out f32 [total_tiles*P, d]   (P = patches per tile; token 0 of a tile is CLS)
+ *   tile_image/tile_slot int32 [total_tiles], image_ar int32 [n_images] (aspect-ratio id)
+ *   cls f32[d]; pos f32[P+1, d]; pos_scale: pos multiplier ((1 - tanh g) for Mllama, 1 for CLIP)
+ *   tile_pos (optional) f32 [n_ar, slots, P+1, d] scaled by tile_pos_scale (tanh g)
+ *   pre_tile (optional) f32 [n_ar, slots, d] added to patch tokens only, scaled by pre_scale.
+ *   resid f32 [total_tiles*(P+1), d] = LN(x; gamma, beta, eps)
+ */
+int mmk_embed_tokens(const float* patch_out, const int32_t* tile_image, const int32_t* tile_slot,
+                     const int32_t* image_ar, int32_t total_tiles, int32_t patches_per_tile,
+                     int32_t d, const float* cls, const float* pos, float pos_scale,
+                     const float* tile_pos, float tile_pos_scale, const float* pre_tile,
+                     float pre_scale, int32_t slots, const float* gamma, const float* beta,
+                     float eps, float* resid, cudaStream_t stream);
+
+/*
+ * K9 — ragged pack into the LLM-prefill buffer.
+ * Mllama: out bf16 [T, d*(1+n_inter)] = [final_f32 -> bf16 | interleaved intermediates]
+ *   where column d + c*n_inter + j = inter[j][t][c]  (HF torch.stack(..., dim=-1) order).
+ */
+int mmk_pack_mllama(const float* final_resid, const void* inter, int32_t n_inter, int32_t rows,
+                    int32_t d, void* out, cudaStream_t stream);
+/*
+ * CLIP/LLaVA: drop the first `drop` tokens of every tile: out bf16 [tiles*(P-drop), d] from
+ * src (bf16 or f32 when src_f32 != 0) [tiles*P, d].
+ */
+int mmk_pack_drop_cls(const void* src, int32_t src_f32, int32_t tiles, int32_t tokens_per_tile,
+                      int32_t drop, int32_t d, void* out, cudaStream_t stream);
+
+/* Element count checksum helper for end-to-end runs: out[0] = sum(float(x)) over n bf16. */
+int mmk_checksum_bf16(const void* x, int64_t n, float* out, cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MMK_H_ */

@@ -1,0 +1,279 @@
+// mmk_gemm.cu — persistent, warp-specialised tcgen05 GEMM with fused epilogues.
+//
+//   D[M, N] = A[M, K] · B[N, K]^T      A, B bf16 K-major (activations · nn.Linear weights)
+//
+// Replaces the modelled `LatencyProfile.encode_latency` (reference
+// pkg/src/lmmsim/profiles.py:136-145) with the encoder's real dense contractions:
+// patch-embed (K2), QKV (K4), O-proj + residual (K6), FC1 + GELU (K7), FC2 + residual (K8).
+//
+// Structure (one CTA per SM, persistent over output tiles):
+//   warp 0      TMA producer: A/B k-blocks -> STAGES-deep smem ring (128B swizzle)
+//   warp 1      MMA issuer:   one thread issues tcgen05.mma (M=128, N=BN, K=16) into TMEM
+//   warp 2      TMEM allocator (2 x BN fp32 columns: double-buffered accumulator)
+//   warps 4..11 epilogue:     tcgen05.ld -> bias / activation / gated residual -> global
+// Epilogue of tile i overlaps the MMAs of tile i+1 via the two accumulator buffers.
+#include "sm100_common.cuh"
+#include "mmk_internal.h"
+
+namespace mmk {
+
+constexpr int kGemmBM = 128;
+constexpr int kGemmBK = 64;
+constexpr int kGemmThreads = 384;  // 4 control warps + 8 epilogue warps
+
+template <int BN, int STAGES>
+struct GemmSmem {
+  static constexpr int kABytes = kGemmBM * kGemmBK * 2;
+  static constexpr int kBBytes = BN * kGemmBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kBarOffset = STAGES * kStageBytes;
+  static constexpr int kTotal = kBarOffset + 256 + 1024;  // + barriers + alignment slack
+};
+
+MMK_DEV float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
+MMK_DEV float quick_gelu(float x) { return x / (1.0f + __expf(-1.702f * x)); }
+
+template <int EPI>
+MMK_DEV float apply_act(float v) {
+  if constexpr (EPI == MMK_EPI_BF16_GELU) return gelu_erf(v);
+  else if constexpr (EPI == MMK_EPI_BF16_QUICKGELU) return quick_gelu(v);
+  else return v;
+}
+
+template <int BN, int STAGES, int EPI>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                  int M, int N, int K, const float* __restrict__ bias, void* __restrict__ out,
+                  int64_t ldo, float gate, __nv_bfloat16* __restrict__ aux, int64_t ld_aux) {
+  using S = GemmSmem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;  // [2]
+  uint64_t* tempty_bar = tfull_bar + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const uint32_t warp = warp_id_uniform();
+  const uint32_t lane = lane_id();
+  const int n_tiles_n = (N + BN - 1) / BN;
+  const int n_tiles_m = (M + kGemmBM - 1) / kGemmBM;
+  const int n_tiles = n_tiles_m * n_tiles_n;
+  const int num_kb = (K + kGemmBK - 1) / kGemmBK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 8);  // one arrive per epilogue warp
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<2 * BN>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint64_t pol_b = l2_policy_evict_last();  // weights: re-read by every M tile
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int m0 = (tile / n_tiles_n) * kGemmBM;
+        const int n0 = (tile % n_tiles_n) * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * S::kStageBytes;
+          uint8_t* sb = sa + S::kABytes;
+          mbar_arrive_expect_tx(&full_bar[stage], S::kStageBytes);
+          tma_load_2d(&tmap_a, &full_bar[stage], sa, kb * kGemmBK, m0);
+          tma_load_2d_hint(&tmap_b, &full_bar[stage], sb, kb * kGemmBK, n0, pol_b);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16_f32(kGemmBM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int t = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
+        const int acc = t & 1;
+        const uint32_t acc_phase = (t >> 1) & 1;
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + stage * S::kStageBytes);
+          const uint32_t b_addr = a_addr + S::kABytes;
+          const uint64_t adesc = umma_desc_sw128_kmajor(a_addr);
+          const uint64_t bdesc = umma_desc_sw128_kmajor(b_addr);
+#pragma unroll
+          for (int k = 0; k < kGemmBK / 16; ++k) {
+            // +32 bytes per K=16 step inside the 128-byte swizzle row (desc unit = 16 B)
+            umma_bf16_ss(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty_bar[stage]);  // frees the smem slot when these MMAs retire
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull_bar[acc]);  // accumulator ready for the epilogue
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const uint32_t q = warp & 3;              // TMEM lane quarter this warp may access
+    const uint32_t half = (warp - 4) >> 2;    // column half of the BN tile
+    constexpr int kColsPerWarp = BN / 2;
+    int t = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
+      const int acc = t & 1;
+      const uint32_t acc_phase = (t >> 1) & 1;
+      const int m0 = (tile / n_tiles_n) * kGemmBM;
+      const int n0 = (tile % n_tiles_n) * BN;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int row = m0 + q * 32 + lane;
+      const bool row_ok = row < M;
+#pragma unroll 1
+      for (int c = 0; c < kColsPerWarp / 32; ++c) {
+        const int col_in_tile = half * kColsPerWarp + c * 32;
+        const int col = n0 + col_in_tile;
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + acc * BN + col_in_tile, r);
+        tmem_ld_wait();
+        if (!row_ok || col >= N) continue;
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        if (bias != nullptr) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + col + i));
+            v[i] += b4.x; v[i + 1] += b4.y; v[i + 2] += b4.z; v[i + 3] += b4.w;
+          }
+        }
+        if constexpr (EPI == MMK_EPI_F32) {
+          float* o = reinterpret_cast<float*>(out) + static_cast<int64_t>(row) * ldo + col;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        } else if constexpr (EPI == MMK_EPI_RESID_F32) {
+          float* o = reinterpret_cast<float*>(out) + static_cast<int64_t>(row) * ldo + col;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            float4 rr = *reinterpret_cast<const float4*>(o + i);
+            rr.x = fmaf(gate, v[i], rr.x);
+            rr.y = fmaf(gate, v[i + 1], rr.y);
+            rr.z = fmaf(gate, v[i + 2], rr.z);
+            rr.w = fmaf(gate, v[i + 3], rr.w);
+            v[i] = rr.x; v[i + 1] = rr.y; v[i + 2] = rr.z; v[i + 3] = rr.w;
+            *reinterpret_cast<float4*>(o + i) = rr;
+          }
+          if (aux != nullptr) {
+            __nv_bfloat16* ao = aux + static_cast<int64_t>(row) * ld_aux + col;
+#pragma unroll
+            for (int i = 0; i < 32; i += 8)
+              st_global_v4(ao + i, pack_bf16x2(v[i], v[i + 1]), pack_bf16x2(v[i + 2], v[i + 3]),
+                           pack_bf16x2(v[i + 4], v[i + 5]), pack_bf16x2(v[i + 6], v[i + 7]));
+          }
+        } else {
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + static_cast<int64_t>(row) * ldo + col;
+#pragma unroll
+          for (int i = 0; i < 32; i += 8)
+            st_global_v4(o + i, pack_bf16x2(apply_act<EPI>(v[i]), apply_act<EPI>(v[i + 1])),
+                         pack_bf16x2(apply_act<EPI>(v[i + 2]), apply_act<EPI>(v[i + 3])),
+                         pack_bf16x2(apply_act<EPI>(v[i + 4]), apply_act<EPI>(v[i + 5])),
+                         pack_bf16x2(apply_act<EPI>(v[i + 6]), apply_act<EPI>(v[i + 7])));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<2 * BN>(tmem_base);
+}
+
+// ------------------------------------------------------------------ host side
+template <int BN, int STAGES, int EPI>
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
+                       const float* bias, void* out, int64_t ldo, float gate, __nv_bfloat16* aux,
+                       int64_t ld_aux, cudaStream_t stream) {
+  using S = GemmSmem<BN, STAGES>;
+  auto kern = gemm_bf16_tcgen05<BN, STAGES, EPI>;
+  static bool attr_done = false;  // per template instance
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
+    if (e != cudaSuccess) return set_cuda_error(e, "gemm: cudaFuncSetAttribute");
+    attr_done = true;
+  }
+  const int tiles = ((M + kGemmBM - 1) / kGemmBM) * ((N + BN - 1) / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  kern<<<grid, kGemmThreads, S::kTotal, stream>>>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "gemm: launch");
+  return MMK_OK;
+}
+
+template <int BN, int STAGES>
+static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
+                        const float* bias, void* out, int64_t ldo, float gate, __nv_bfloat16* aux,
+                        int64_t ld_aux, cudaStream_t s) {
+  switch (epi) {
+    case MMK_EPI_BF16: return launch_gemm<BN, STAGES, MMK_EPI_BF16>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
+    case MMK_EPI_BF16_GELU: return launch_gemm<BN, STAGES, MMK_EPI_BF16_GELU>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
+    case MMK_EPI_BF16_QUICKGELU: return launch_gemm<BN, STAGES, MMK_EPI_BF16_QUICKGELU>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
+    case MMK_EPI_F32: return launch_gemm<BN, STAGES, MMK_EPI_F32>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
+    case MMK_EPI_RESID_F32: return launch_gemm<BN, STAGES, MMK_EPI_RESID_F32>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
+    default: return set_error(MMK_ERR_ARG, "gemm: unknown epilogue %d", epi);
+  }
+}
+
+}  // namespace mmk
+
+using namespace mmk;
+
+extern "C" int mmk_gemm_bf16(const void* a, int64_t lda, const void* b, int64_t ldb, int32_t m,
+                             int32_t n, int32_t k, int32_t epilogue, const float* bias, void* out,
+                             int64_t ldo, float gate, void* aux, int64_t ld_aux, cudaStream_t stream) {
+  if (m < 0 || n <= 0 || k <= 0) return set_error(MMK_ERR_ARG, "gemm: bad shape m=%d n=%d k=%d", m, n, k);
+  if (m == 0) return MMK_OK;
+  if (n % 32 != 0) return set_error(MMK_ERR_UNSUPPORTED, "gemm: N=%d must be a multiple of 32", n);
+  if (lda % 8 != 0 || ldb % 8 != 0 || lda < k || ldb < k)
+    return set_error(MMK_ERR_ARG, "gemm: lda/ldb must be >= K and multiples of 8 elements");
+  if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return set_error(MMK_ERR_ARG, "gemm: pointers must be 16-byte aligned");
+  const bool f32_out = epilogue == MMK_EPI_F32 || epilogue == MMK_EPI_RESID_F32;
+  if (ldo % (f32_out ? 4 : 8) != 0) return set_error(MMK_ERR_ARG, "gemm: ldo misaligned");
+  if (aux != nullptr && (epilogue != MMK_EPI_RESID_F32 || ld_aux % 8 != 0))
+    return set_error(MMK_ERR_ARG, "gemm: aux output only with RESID_F32 and 16B-aligned rows");
+  // BN choice: 256 unless that leaves most SMs idle.
+  const int tiles256 = ((m + kGemmBM - 1) / kGemmBM) * ((n + 255) / 256);
+  const bool use128 = (n % 256 != 0) || tiles256 < num_sms();
+  CUtensorMap ta, tb;
+  int rc = make_tmap_2d_bf16(&ta, a, k, m, lda, kGemmBK, kGemmBM, /*swizzle128=*/true);
+  if (rc) return rc;
+  rc = make_tmap_2d_bf16(&tb, b, k, n, ldb, kGemmBK, use128 ? 128 : 256, true);
+  if (rc) return rc;
+  if (use128)
+    return dispatch_epi<128, 6>(epilogue, ta, tb, m, n, k, bias, out, ldo, gate,
+                                reinterpret_cast<__nv_bfloat16*>(aux), ld_aux, stream);
+  return dispatch_epi<256, 4>(epilogue, ta, tb, m, n, k, bias, out, ldo, gate,
+                              reinterpret_cast<__nv_bfloat16*>(aux), ld_aux, stream);
+}

@@ -1,0 +1,22 @@
+// mmk_internal.h — shared host-side helpers of libmmk (error state, SM count, TMA maps).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include "mmk.h"
+
+namespace mmk {
+
+int set_error(int code, const char* fmt, ...);
+int set_cuda_error(cudaError_t e, const char* where);
+int num_sms();
+
+// 2-D bf16 tensor map over a row-major [rows, inner] matrix with row pitch `ld` elements,
+// box = {box_inner, box_rows}; 128-byte swizzle (box_inner*2 must be 128) or none.
+int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows,
+                      uint64_t ld, uint32_t box_inner, uint32_t box_rows, bool swizzle128);
+// Generic encoder (rank <= 5), strides in bytes for dims 1..rank-1.
+int make_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
+                   const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swz);
+
+}  // namespace mmk
