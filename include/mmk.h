@@ -53,14 +53,22 @@ const char* mmk_last_error(void);
  * (core.py:110-120) for n images at once, and adds the pixel geometry of each image.
  *   in : w[n], h[n] (int32 pixels, >= 1), tile edge T, tokens/tile, cap, thumbnail flag
  *   out: tiles[n]; tile_off[n+1], tok_off[n+1] (int64 exclusive prefix sums);
- *        geom[n*4] = {rows, cols, resized_w, resized_h} of the tile canvas;
+ *        geom[n*4] = {rows, cols, resized_w, resized_h} of the tile canvas
+ *        (resize_mode 0: Mllama canvas fit; 1: CLIP shortest-side resize, crop later);
+ *        ar_id[n] (optional) = 1 + index of (rows, cols) in the enumeration of all (a, b) with
+ *        a*b <= cap, a outer (transformers Mllama supported_aspect_ratios; 0 = no image);
  *        bad[1] (int32) = number of images with w<1 or h<1 (their tiles are 0).
  * Single launch, one CTA, n <= 65536.
  */
 int mmk_tile_plan(const int32_t* w, const int32_t* h, int32_t n, int32_t tile_px,
-                  int32_t tokens_per_tile, int32_t max_tiles, int32_t thumbnail, int32_t* tiles,
-                  int64_t* tile_off, int64_t* tok_off, int32_t* geom, int32_t* bad,
-                  cudaStream_t stream);
+                  int32_t tokens_per_tile, int32_t max_tiles, int32_t thumbnail,
+                  int32_t resize_mode, int32_t* tiles,
+                  int64_t* tile_off, int64_t* tok_off, int32_t* geom, int32_t* ar_id,
+                  int32_t* bad, cudaStream_t stream);
+
+/* Per-tile (image index, slot inside the image) from tile_off[n+1]; outputs sized total_tiles. */
+int mmk_tile_index(const int64_t* tile_off, int32_t n, int32_t* tile_image, int32_t* tile_slot,
+                   cudaStream_t stream);
 
 /*
  * K1 — fused uint8 HWC -> resize (bilinear, fp32) -> pad -> normalize -> tile -> patchify.
@@ -91,13 +99,14 @@ int mmk_gemm_bf16(const void* a, int64_t lda, const void* b, int64_t ldb, int32_
 /*
  * K3 — row LayerNorm: y_bf16 = LN(x_f32) * gamma + beta (+ optional per-tile additive term).
  *   x f32 [rows, d]; y bf16 [rows, d] (or f32 when y_f32 != 0, may alias x).
- *   tile_add (optional, f32 [n_tables, slots, d]) : y += tile_add[table[tile], slot[tile]]
- *   where tile = row / rows_per_tile; tile_table/tile_slot int32 [n_tiles].
+ *   tile_add (optional, f32 [n_tables, slots, d]) :
+ *       y += tile_add[image_table[tile_image[tile]], tile_slot[tile]],  tile = row / rows_per_tile
+ *   (tile_image/tile_slot int32 [n_tiles], image_table int32 [n_images]).
  */
 int mmk_layernorm(const float* x, void* y, int32_t y_f32, int32_t rows, int32_t d,
                   const float* gamma, const float* beta, float eps, const float* tile_add,
-                  const int32_t* tile_table, const int32_t* tile_slot, int32_t rows_per_tile,
-                  int32_t slots, cudaStream_t stream);
+                  const int32_t* tile_image, const int32_t* image_table, const int32_t* tile_slot,
+                  int32_t rows_per_tile, int32_t slots, cudaStream_t stream);
 
 /*
  * K5 — non-causal variable-length multi-head self-attention (one sequence per image).

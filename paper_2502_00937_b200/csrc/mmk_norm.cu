@@ -1,0 +1,296 @@
+// mmk_norm.cu — HBM-bound row kernels of the encoder:
+//   K3  LayerNorm over the fp32 residual stream -> bf16 GEMM operand (optionally + per-tile
+//       additive embedding: Mllama layernorm_post + post_tile_positional_embedding)
+//   embedding assembly (class token, gated position / tile-position embeddings, layernorm_pre)
+//   K9  ragged pack of final + intermediate hidden states into the LLM-prefill buffer
+// One warp per row, float4 loads, statistics in fp32 (two-pass mean / variance in registers).
+#include "sm100_common.cuh"
+#include "mmk_internal.h"
+
+namespace mmk {
+
+MMK_DEV float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Normalise the VEC float4 of this lane (columns lane*4 + j*128) in place.
+template <int VEC>
+MMK_DEV void ln_inplace(float4 (&x)[VEC], int d, const float* __restrict__ gamma, const float* __restrict__ beta,
+                        float eps, int lane) {
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) s += (x[j].x + x[j].y) + (x[j].z + x[j].w);
+  const float mean = warp_sum(s) / d;
+  float q = 0.f;
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) {
+    const float a = x[j].x - mean, b = x[j].y - mean, c = x[j].z - mean, e = x[j].w - mean;
+    q += (a * a + b * b) + (c * c + e * e);
+  }
+  const float rstd = rsqrtf(warp_sum(q) / d + eps);
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) {
+    const int col = lane * 4 + j * 128;
+    const float4 g = __ldg(reinterpret_cast<const float4*>(gamma + col));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(beta + col));
+    x[j].x = (x[j].x - mean) * rstd * g.x + b.x;
+    x[j].y = (x[j].y - mean) * rstd * g.y + b.y;
+    x[j].z = (x[j].z - mean) * rstd * g.z + b.z;
+    x[j].w = (x[j].w - mean) * rstd * g.w + b.w;
+  }
+}
+
+template <int VEC>
+MMK_DEV void store_row(void* y, int y_f32, int64_t row, int d, const float4 (&x)[VEC], int lane) {
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) {
+    const int col = lane * 4 + j * 128;
+    if (y_f32) {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + row * d + col) = x[j];
+    } else {
+      uint2 v;
+      v.x = pack_bf16x2(x[j].x, x[j].y);
+      v.y = pack_bf16x2(x[j].z, x[j].w);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(y) + row * d + col) = v;
+    }
+  }
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(256)
+layernorm_kernel(const float* __restrict__ x, void* y, int y_f32, int rows, int d, const float* __restrict__ gamma,
+                 const float* __restrict__ beta, float eps, const float* __restrict__ tile_add,
+                 const int32_t* __restrict__ tile_image, const int32_t* __restrict__ image_table,
+                 const int32_t* __restrict__ tile_slot, int rows_per_tile, int slots) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  float4 v[VEC];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) v[j] = *reinterpret_cast<const float4*>(x + row * d + lane * 4 + j * 128);
+  ln_inplace<VEC>(v, d, gamma, beta, eps, lane);
+  if (tile_add != nullptr) {
+    const int64_t tile = row / rows_per_tile;
+    const float* add = tile_add + (static_cast<int64_t>(image_table[tile_image[tile]]) * slots + tile_slot[tile]) * d;
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(add + lane * 4 + j * 128));
+      v[j].x += a.x; v[j].y += a.y; v[j].z += a.z; v[j].w += a.w;
+    }
+  }
+  store_row<VEC>(y, y_f32, row, d, v, lane);
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(256)
+embed_kernel(const float* __restrict__ patch_out, const int32_t* __restrict__ tile_image,
+             const int32_t* __restrict__ tile_slot, const int32_t* __restrict__ image_ar, int total_tiles, int P, int d,
+             const float* __restrict__ cls, const float* __restrict__ pos, float pos_scale,
+             const float* __restrict__ tile_pos, float tile_pos_scale, const float* __restrict__ pre_tile,
+             float pre_scale, int slots, const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
+             float* __restrict__ resid) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int64_t rows = static_cast<int64_t>(total_tiles) * (P + 1);
+  if (row >= rows) return;
+  const int g = static_cast<int>(row / (P + 1));
+  const int p = static_cast<int>(row - static_cast<int64_t>(g) * (P + 1));
+  const int ar = image_ar ? image_ar[tile_image[g]] : 0;
+  const int slot = tile_slot ? tile_slot[g] : 0;
+  float4 v[VEC];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) {
+    const int col = lane * 4 + j * 128;
+    float4 a;
+    if (p == 0) {
+      a = __ldg(reinterpret_cast<const float4*>(cls + col));
+    } else {
+      a = *reinterpret_cast<const float4*>(patch_out + (static_cast<int64_t>(g) * P + (p - 1)) * d + col);
+      if (pre_tile != nullptr) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(pre_tile + (static_cast<int64_t>(ar) * slots + slot) * d + col));
+        a.x += pre_scale * t.x; a.y += pre_scale * t.y; a.z += pre_scale * t.z; a.w += pre_scale * t.w;
+      }
+    }
+    const float4 ps = __ldg(reinterpret_cast<const float4*>(pos + static_cast<int64_t>(p) * d + col));
+    a.x += pos_scale * ps.x; a.y += pos_scale * ps.y; a.z += pos_scale * ps.z; a.w += pos_scale * ps.w;
+    if (tile_pos != nullptr) {
+      const float4 t = __ldg(reinterpret_cast<const float4*>(
+          tile_pos + ((static_cast<int64_t>(ar) * slots + slot) * (P + 1) + p) * d + col));
+      a.x += tile_pos_scale * t.x; a.y += tile_pos_scale * t.y; a.z += tile_pos_scale * t.z; a.w += tile_pos_scale * t.w;
+    }
+    v[j] = a;
+  }
+  ln_inplace<VEC>(v, d, gamma, beta, eps, lane);
+  store_row<VEC>(resid, 1, row, d, v, lane);
+}
+
+// One CTA per token row: final fp32 -> bf16 columns [0, d); intermediates interleaved
+// (column d + c*n_inter + j = inter[j][row][c]) staged through shared memory so that both
+// the gather and the 16-byte stores are coalesced.
+__global__ void __launch_bounds__(128)
+pack_mllama_kernel(const float* __restrict__ fin, const __nv_bfloat16* __restrict__ inter, int n_inter, int rows,
+                   int d, __nv_bfloat16* __restrict__ out) {
+  extern __shared__ __align__(16) __nv_bfloat16 s_inter[];  // [n_inter][d]
+  const int64_t row = blockIdx.x;
+  const int64_t ldo = static_cast<int64_t>(d) * (1 + n_inter);
+  for (int j = 0; j < n_inter; ++j)
+    for (int c = threadIdx.x * 8; c < d; c += 128 * 8)
+      *reinterpret_cast<uint4*>(s_inter + j * d + c) =
+          *reinterpret_cast<const uint4*>(inter + (static_cast<int64_t>(j) * rows + row) * d + c);
+  __nv_bfloat16* o = out + row * ldo;
+  for (int c = threadIdx.x * 8; c < d; c += 128 * 8) {
+    const float4 a = *reinterpret_cast<const float4*>(fin + row * d + c);
+    const float4 b = *reinterpret_cast<const float4*>(fin + row * d + c + 4);
+    st_global_v4(o + c, pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y), pack_bf16x2(b.z, b.w));
+  }
+  __syncthreads();
+  const int span = d * n_inter;
+  for (int e = threadIdx.x * 8; e < span; e += 128 * 8) {
+    uint32_t w4[4];
+#pragma unroll
+    for (int u = 0; u < 8; u += 2) {
+      const int e0 = e + u, e1 = e + u + 1;
+      const __nv_bfloat16 v0 = s_inter[(e0 % n_inter) * d + e0 / n_inter];
+      const __nv_bfloat16 v1 = s_inter[(e1 % n_inter) * d + e1 / n_inter];
+      w4[u / 2] = static_cast<uint32_t>(__bfloat16_as_ushort(v0)) | (static_cast<uint32_t>(__bfloat16_as_ushort(v1)) << 16);
+    }
+    st_global_v4(o + d + e, w4[0], w4[1], w4[2], w4[3]);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+pack_drop_kernel(const void* __restrict__ src, int src_f32, int64_t out_rows, int tokens_per_tile, int drop, int d,
+                 __nv_bfloat16* __restrict__ out) {
+  const int keep = tokens_per_tile - drop;
+  const int64_t orow = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (orow >= out_rows) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t tile = orow / keep;
+  const int64_t srow = tile * tokens_per_tile + drop + (orow - tile * keep);
+  for (int c = lane * 8; c < d; c += 256) {
+    if (src_f32) {
+      const float* s = reinterpret_cast<const float*>(src) + srow * d + c;
+      const float4 a = *reinterpret_cast<const float4*>(s);
+      const float4 b = *reinterpret_cast<const float4*>(s + 4);
+      st_global_v4(out + orow * d + c, pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y),
+                   pack_bf16x2(b.z, b.w));
+    } else {
+      *reinterpret_cast<uint4*>(out + orow * d + c) =
+          *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(src) + srow * d + c);
+    }
+  }
+}
+
+__global__ void checksum_kernel(const __nv_bfloat16* __restrict__ x, int64_t n, float* out) {
+  float s = 0.f;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    s += __bfloat162float(x[i]);
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
+}
+
+
+static int grid_rows(int64_t rows) { return static_cast<int>((rows + 7) / 8); }
+
+}  // namespace mmk
+
+using namespace mmk;
+
+#define MMK_LN_CASE(V)                                                                                       \
+  case V:                                                                                                    \
+    layernorm_kernel<V><<<grid_rows(rows), 256, 0, stream>>>(x, y, y_f32, rows, d, gamma, beta, eps, tile_add, \
+                                                             tile_image, image_table, tile_slot, rows_per_tile, \
+                                                             slots);                                            \
+    break;
+
+extern "C" int mmk_layernorm(const float* x, void* y, int32_t y_f32, int32_t rows, int32_t d, const float* gamma,
+                             const float* beta, float eps, const float* tile_add, const int32_t* tile_image,
+                             const int32_t* image_table, const int32_t* tile_slot, int32_t rows_per_tile,
+                             int32_t slots, cudaStream_t stream) {
+  if (rows < 0 || d <= 0) return set_error(MMK_ERR_ARG, "layernorm: bad shape");
+  if (rows == 0) return MMK_OK;
+  if (tile_add && (rows_per_tile <= 0 || !tile_image || !image_table || !tile_slot))
+    return set_error(MMK_ERR_ARG, "layernorm: tile_add needs tile_image/image_table/tile_slot/rows_per_tile");
+  switch (d / 128 * (d % 128 == 0)) {
+    MMK_LN_CASE(4)
+    MMK_LN_CASE(6)
+    MMK_LN_CASE(8)
+    MMK_LN_CASE(10)
+    MMK_LN_CASE(12)
+    MMK_LN_CASE(16)
+    default: return set_error(MMK_ERR_UNSUPPORTED, "layernorm: d=%d unsupported", d);
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "layernorm: launch");
+}
+
+#define MMK_EMB_CASE(V)                                                                                   \
+  case V:                                                                                                 \
+    embed_kernel<V><<<grid_rows(rows), 256, 0, stream>>>(patch_out, tile_image, tile_slot, image_ar,      \
+                                                         total_tiles, patches_per_tile, d, cls, pos,       \
+                                                         pos_scale, tile_pos, tile_pos_scale, pre_tile,    \
+                                                         pre_scale, slots, gamma, beta, eps, resid);       \
+    break;
+
+extern "C" int mmk_embed_tokens(const float* patch_out, const int32_t* tile_image, const int32_t* tile_slot,
+                                const int32_t* image_ar, int32_t total_tiles, int32_t patches_per_tile, int32_t d,
+                                const float* cls, const float* pos, float pos_scale, const float* tile_pos,
+                                float tile_pos_scale, const float* pre_tile, float pre_scale, int32_t slots,
+                                const float* gamma, const float* beta, float eps, float* resid,
+                                cudaStream_t stream) {
+  if (total_tiles < 0 || patches_per_tile <= 0 || d <= 0) return set_error(MMK_ERR_ARG, "embed: bad shape");
+  if ((tile_pos || pre_tile) && (!tile_image || !tile_slot || !image_ar))
+    return set_error(MMK_ERR_ARG, "embed: tile embeddings need tile_image/tile_slot/image_ar");
+  const int64_t rows = static_cast<int64_t>(total_tiles) * (patches_per_tile + 1);
+  if (rows == 0) return MMK_OK;
+  switch (d / 128 * (d % 128 == 0)) {
+    MMK_EMB_CASE(4)
+    MMK_EMB_CASE(6)
+    MMK_EMB_CASE(8)
+    MMK_EMB_CASE(10)
+    MMK_EMB_CASE(12)
+    MMK_EMB_CASE(16)
+    default: return set_error(MMK_ERR_UNSUPPORTED, "embed: d=%d unsupported", d);
+  }
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "embed: launch");
+}
+
+extern "C" int mmk_pack_mllama(const float* final_resid, const void* inter, int32_t n_inter, int32_t rows, int32_t d,
+                               void* out, cudaStream_t stream) {
+  if (rows < 0 || d <= 0 || n_inter < 0 || d % 8 != 0) return set_error(MMK_ERR_ARG, "pack_mllama: bad shape");
+  if (rows == 0) return MMK_OK;
+  const int smem = n_inter * d * 2;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(pack_mllama_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return set_cuda_error(e, "pack_mllama: smem attr");
+  }
+  pack_mllama_kernel<<<rows, 128, smem, stream>>>(final_resid, reinterpret_cast<const __nv_bfloat16*>(inter), n_inter,
+                                                  rows, d, reinterpret_cast<__nv_bfloat16*>(out));
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "pack_mllama: launch");
+}
+
+extern "C" int mmk_pack_drop_cls(const void* src, int32_t src_f32, int32_t tiles, int32_t tokens_per_tile,
+                                 int32_t drop, int32_t d, void* out, cudaStream_t stream) {
+  if (tiles < 0 || tokens_per_tile <= drop || drop < 0 || d % 8 != 0) return set_error(MMK_ERR_ARG, "pack_drop: bad shape");
+  const int64_t out_rows = static_cast<int64_t>(tiles) * (tokens_per_tile - drop);
+  if (out_rows == 0) return MMK_OK;
+  pack_drop_kernel<<<grid_rows(out_rows), 256, 0, stream>>>(src, src_f32, out_rows, tokens_per_tile, drop, d,
+                                                            reinterpret_cast<__nv_bfloat16*>(out));
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "pack_drop: launch");
+}
+
+extern "C" int mmk_checksum_bf16(const void* x, int64_t n, float* out, cudaStream_t stream) {
+  if (n < 0) return set_error(MMK_ERR_ARG, "checksum: n < 0");
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(float), stream);
+  if (e != cudaSuccess) return set_cuda_error(e, "checksum: memset");
+  if (n == 0) return MMK_OK;
+  checksum_kernel<<<4 * num_sms(), 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(x), n, out);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "checksum: launch");
+}

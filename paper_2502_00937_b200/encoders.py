@@ -1,0 +1,202 @@
+"""Vision encoders of the image path, executed as libmmk kernels on one B200.
+
+Replaces the modelled encode stage (reference LatencyProfile.encode_latency,
+pkg/src/lmmsim/profiles.py:136-145, called from engine.py:693-703) with the real forward:
+
+  patches -> K2 patch GEMM -> embedding assembly + LN_pre -> L x [ K3 LN -> K4 QKV GEMM ->
+  K5 varlen attention -> K6 O-proj GEMM + (gated) residual -> K3 LN -> K7 FC1 GEMM + GELU ->
+  K8 FC2 GEMM + (gated) residual (+ intermediate capture) ] -> K9 pack
+
+Families (EncoderSpec.family):
+* "clip"   pre-LN ViT (ViT-B/16-224, CLIP ViT-L/14-336 as used by LLaVA: layer -2, no CLS)
+* "mllama" Llama-3.2-Vision encoder: gated tile embeddings, 32 local + 8 gated global layers,
+           output = [final | interleaved hidden_states[3,7,15,23,30]] (7680 wide)
+
+Residual stream in fp32 (HBM), GEMM operands in bf16, fp32 accumulation in TMEM.
+Weights are random-initialised from a seed (no checkpoints in this environment).
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import ops
+from .core import ModelSpec, SpecError
+
+K_ALIGN = 16  # patch vectors are zero-padded to a multiple of 16 elements (TMA row pitch)
+
+
+def k_pad_of(spec: ModelSpec) -> int:
+    k = 3 * spec.encoder.patch_px ** 2
+    return -(-k // K_ALIGN) * K_ALIGN
+
+
+def _bf16_exact(t: torch.Tensor) -> torch.Tensor:
+    return t.to(torch.bfloat16).to(torch.float32)
+
+
+def init_weights(spec: ModelSpec, seed: int = 0, gate_scale: float = 0.5) -> dict:
+    """Seeded random init (float32 CPU).  GEMM weights are rounded to bf16 values so the fp32
+    oracle and the bf16 device path use numerically identical weights.  Unlike HF's init, gates
+    and biases are non-zero so every term of the forward is exercised."""
+    enc = spec.encoder
+    if enc is None:
+        raise SpecError(f"{spec.name}: no encoder block in the model spec")
+    g = torch.Generator().manual_seed(seed)
+    d, ff = enc.hidden, enc.ffn
+    P = (spec.tile_edge_px // enc.patch_px) ** 2
+    std = 0.02
+
+    def nrm(*shape, s=std):
+        return torch.randn(*shape, generator=g) * s
+
+    W: dict = {}
+    W["patch_w"] = _bf16_exact(nrm(d, 3 * enc.patch_px ** 2))
+    W["cls"] = nrm(d, s=d ** -0.5)
+    W["pos"] = nrm(P + 1, d, s=d ** -0.5)
+    for nm in ("pre_ln", "post_ln"):
+        W[nm + "_w"] = 1.0 + nrm(d)
+        W[nm + "_b"] = nrm(d)
+
+    def block(pre: str, gated: bool):
+        W[pre + "ln1_w"] = 1.0 + nrm(d)
+        W[pre + "ln1_b"] = nrm(d)
+        W[pre + "qkv_w"] = _bf16_exact(nrm(3 * d, d))
+        W[pre + "qkv_b"] = nrm(3 * d) if enc.qkv_bias else None
+        W[pre + "o_w"] = _bf16_exact(nrm(d, d))
+        W[pre + "o_b"] = nrm(d) if enc.qkv_bias else None
+        W[pre + "ln2_w"] = 1.0 + nrm(d)
+        W[pre + "ln2_b"] = nrm(d)
+        W[pre + "fc1_w"] = _bf16_exact(nrm(ff, d))
+        W[pre + "fc1_b"] = nrm(ff)
+        W[pre + "fc2_w"] = _bf16_exact(nrm(d, ff))
+        W[pre + "fc2_b"] = nrm(d)
+        if gated:
+            W[pre + "gate_attn"] = torch.randn(1, generator=g) * gate_scale + math.pi / 4
+            W[pre + "gate_ffn"] = torch.randn(1, generator=g) * gate_scale + math.pi / 4
+
+    for i in range(enc.layers):
+        block(f"l{i}.", False)
+    if enc.family == "mllama":
+        n_ar = enc.num_aspect_ratios + 1
+        slots = spec.max_tiles_per_image
+        for i in range(enc.global_layers):
+            block(f"g{i}.", True)
+        W["pos_gate"] = torch.randn(1, generator=g) * gate_scale
+        W["pre_gate"] = torch.randn(1, generator=g) * gate_scale
+        W["post_gate"] = torch.randn(1, generator=g) * gate_scale
+        W["tile_pos"] = nrm(n_ar, slots, P + 1, d)
+        W["pre_tile"] = nrm(n_ar, slots, d)
+        W["post_tile"] = nrm(n_ar, slots, d)
+    return W
+
+
+class DeviceEncoder:
+    """Device-resident weights + the forward of one encoder over a ragged batch of tiles."""
+
+    def __init__(self, spec: ModelSpec, weights: dict, device="cuda"):
+        enc = spec.encoder
+        if enc is None:
+            raise SpecError(f"{spec.name}: no encoder block")
+        if enc.head_dim not in (64, 80):
+            from ._lib import ProfileError
+            raise ProfileError(f"{spec.name}: head_dim {enc.head_dim} not supported by the attention kernel")
+        self.spec, self.enc, self.device = spec, enc, torch.device(device)
+        self.P = (spec.tile_edge_px // enc.patch_px) ** 2
+        self.k_pad = k_pad_of(spec)
+        dev = self.device
+        bf = lambda t: t.to(dev, torch.bfloat16).contiguous()  # noqa: E731
+        f32 = lambda t: None if t is None else t.to(dev, torch.float32).contiguous()  # noqa: E731
+        d = enc.hidden
+        pw = torch.zeros(d, self.k_pad)
+        pw[:, :weights["patch_w"].shape[1]] = weights["patch_w"]
+        self.patch_w = bf(pw)
+        self.cls, self.pos = f32(weights["cls"]), f32(weights["pos"])
+        self.pre_ln = (f32(weights["pre_ln_w"]), f32(weights["pre_ln_b"]))
+        self.post_ln = (f32(weights["post_ln_w"]), f32(weights["post_ln_b"]))
+
+        def block(pre, gated):
+            return {
+                "ln1": (f32(weights[pre + "ln1_w"]), f32(weights[pre + "ln1_b"])),
+                "qkv_w": bf(weights[pre + "qkv_w"]), "qkv_b": f32(weights.get(pre + "qkv_b")),
+                "o_w": bf(weights[pre + "o_w"]), "o_b": f32(weights.get(pre + "o_b")),
+                "ln2": (f32(weights[pre + "ln2_w"]), f32(weights[pre + "ln2_b"])),
+                "fc1_w": bf(weights[pre + "fc1_w"]), "fc1_b": f32(weights[pre + "fc1_b"]),
+                "fc2_w": bf(weights[pre + "fc2_w"]), "fc2_b": f32(weights[pre + "fc2_b"]),
+                "gate_attn": math.tanh(float(weights[pre + "gate_attn"])) if gated else 1.0,
+                "gate_ffn": math.tanh(float(weights[pre + "gate_ffn"])) if gated else 1.0,
+            }
+
+        self.layers = [block(f"l{i}.", False) for i in range(enc.layers)]
+        self.global_layers = [block(f"g{i}.", True) for i in range(enc.global_layers)]
+        if enc.family == "mllama":
+            tpos = math.tanh(float(weights["pos_gate"]))
+            self.pos_scale, self.tile_pos_scale = 1.0 - tpos, tpos
+            self.pre_scale = math.tanh(float(weights["pre_gate"]))
+            self.tile_pos = f32(weights["tile_pos"])
+            self.pre_tile = f32(weights["pre_tile"])
+            # post-tile embedding folded with its gate: added inside the LN_post kernel
+            self.post_tile_scaled = f32(weights["post_tile"] * math.tanh(float(weights["post_gate"])))
+            self.slots = weights["tile_pos"].shape[1]
+        mean = torch.tensor(enc.mean, dtype=torch.float64)
+        std = torch.tensor(enc.std, dtype=torch.float64)
+        self.norm_scale = (1.0 / (255.0 * std)).to(torch.float32).to(dev)
+        self.norm_shift = (-mean / std).to(torch.float32).to(dev)
+
+    # ------------------------------------------------------------------ layers
+    def _block(self, L, resid, x_buf, qkv_buf, h_buf, cu, n_seq, max_s, aux=None):
+        enc = self.enc
+        ops.layernorm(resid, *L["ln1"], enc.norm_eps, out=x_buf)
+        ops.gemm(x_buf, L["qkv_w"], ops.EPI_BF16, bias=L["qkv_b"], out=qkv_buf)
+        ops.attention(qkv_buf, cu, n_seq, max_s, enc.heads, enc.head_dim, out=x_buf)
+        ops.gemm(x_buf, L["o_w"], ops.EPI_RESID_F32, bias=L["o_b"], out=resid, gate=L["gate_attn"])
+        ops.layernorm(resid, *L["ln2"], enc.norm_eps, out=x_buf)
+        ops.gemm(x_buf, L["fc1_w"], ops.ACT_EPI[enc.act], bias=L["fc1_b"], out=h_buf)
+        ops.gemm(h_buf, L["fc2_w"], ops.EPI_RESID_F32, bias=L["fc2_b"], out=resid, gate=L["gate_ffn"], aux=aux)
+
+    def forward(self, patches: torch.Tensor, total_tiles: int, cu_seqlens: torch.Tensor, n_seq: int, max_seqlen: int,
+                tile_image=None, tile_slot=None, image_ar=None) -> torch.Tensor:
+        """patches [total_tiles*P, k_pad] bf16 -> packed embeddings for the LLM prefill.
+        cu_seqlens int32 [n_seq+1] token offsets of the attention sequences (one per image)."""
+        enc, P, d = self.enc, self.P, self.enc.hidden
+        dev = patches.device
+        T = total_tiles * (P + 1)
+        patch_out = ops.gemm(patches, self.patch_w, ops.EPI_F32)
+        if enc.family == "mllama":
+            resid = ops.embed_tokens(patch_out, total_tiles, P, self.cls, self.pos, self.pos_scale, *self.pre_ln,
+                                     enc.norm_eps, tile_image=tile_image, tile_slot=tile_slot, image_ar=image_ar,
+                                     tile_pos=self.tile_pos, tile_pos_scale=self.tile_pos_scale,
+                                     pre_tile=self.pre_tile, pre_scale=self.pre_scale, slots=self.slots)
+        else:
+            resid = ops.embed_tokens(patch_out, total_tiles, P, self.cls, self.pos, 1.0, *self.pre_ln, enc.norm_eps)
+        del patch_out
+        x_buf = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
+        qkv_buf = torch.empty(T, 3 * d, dtype=torch.bfloat16, device=dev)
+        h_buf = torch.empty(T, enc.ffn, dtype=torch.bfloat16, device=dev)
+        if enc.family == "clip":
+            n_run = enc.layers if enc.out_layer == -1 else enc.layers + 1 + enc.out_layer
+            for L in self.layers[:n_run]:
+                self._block(L, resid, x_buf, qkv_buf, h_buf, cu_seqlens, n_seq, max_seqlen)
+            drop = 1 if enc.drop_cls else 0
+            if enc.out_layer == -1:
+                ops.layernorm(resid, *self.post_ln, enc.norm_eps, out=x_buf)
+                return x_buf if drop == 0 else ops.pack_drop_cls(x_buf, total_tiles, P + 1, drop)
+            return ops.pack_drop_cls(resid, total_tiles, P + 1, drop)
+        # ---------------- mllama
+        outs = list(enc.out_layers)
+        if 0 in outs:
+            raise SpecError("mllama out_layers must be >= 1 (hidden_states[0] capture unsupported)")
+        inter = torch.empty(len(outs), T, d, dtype=torch.bfloat16, device=dev)
+        for i, L in enumerate(self.layers):
+            aux = inter[outs.index(i + 1)] if (i + 1) in outs else None
+            self._block(L, resid, x_buf, qkv_buf, h_buf, cu_seqlens, n_seq, max_seqlen, aux=aux)
+        # layernorm_post + gated post-tile positional embedding, in place on the fp32 stream
+        ops.layernorm(resid, *self.post_ln, enc.norm_eps, out=resid, out_f32=True, tile_add=self.post_tile_scaled,
+                      tile_image=tile_image, image_table=image_ar, tile_slot=tile_slot, rows_per_tile=P + 1,
+                      slots=self.slots)
+        for L in self.global_layers:
+            self._block(L, resid, x_buf, qkv_buf, h_buf, cu_seqlens, n_seq, max_seqlen)
+        del x_buf, qkv_buf, h_buf
+        return ops.pack_mllama(resid, inter)

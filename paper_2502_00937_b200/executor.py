@@ -1,0 +1,159 @@
+"""ImagePathExecutor — the drop-in for the reference's modelled image stages.
+
+In the reference simulator an image shard flows CPU lane -> GPU lane -> handoff:
+``preprocess_latency`` (profiles.py:128-134, engine.py:639-657), then ``encode_latency``
+(profiles.py:136-145, engine.py:682-716), then the shard join (engine.py:730-752) and the
+transfer delay (engine.py:563-579).  Here the same batch objects (``WorkItem`` from
+``form_batch``) are executed for real on one B200:
+
+  stage (H2D of uint8 images) -> K0 tile plan -> K1 preprocess -> encoder (K2-K8) -> K9 pack
+
+and the result is the packed prefill buffer [sum(image_tokens), D_out] bf16 plus int64
+token offsets — exactly ``Request.total_image_tokens`` rows (core.py:110-112) per request.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import ops
+from .batcher import WorkItem
+from .core import ModelSpec, SpecError, StageKind, tile_count
+from .encoders import DeviceEncoder, init_weights
+
+
+@dataclass
+class ImageBatch:
+    """Raw images staged on the device: one flat uint8 HWC buffer + per-image metadata."""
+
+    src: torch.Tensor          # uint8 [sum(h*w*3)]
+    src_off: torch.Tensor      # int64 [n] byte offsets
+    w: torch.Tensor            # int32 [n]
+    h: torch.Tensor            # int32 [n]
+    dims: list                 # host [(w, h)]
+    h2d_bytes: int = 0
+
+    @property
+    def n(self) -> int:
+        return len(self.dims)
+
+
+@dataclass
+class PackedBatch:
+    embeds: torch.Tensor                 # bf16 [sum tokens, D_out]  (LLM-prefill layout)
+    tok_offsets: torch.Tensor            # int64 [n+1] device (from K0)
+    tiles: list[int]                     # host, per image
+    image_tokens: list[int]              # host, per image
+    item_spans: dict = field(default_factory=dict)  # WorkItem.seq -> (first image, end image)
+
+    @property
+    def total_tokens(self) -> int:
+        return int(sum(self.image_tokens))
+
+
+def _as_hwc_u8(img) -> np.ndarray | torch.Tensor:
+    if isinstance(img, torch.Tensor):
+        if img.dtype != torch.uint8 or img.dim() != 3 or img.shape[2] != 3:
+            raise SpecError("images must be uint8 HWC tensors with 3 channels")
+        return img
+    a = np.asarray(img)
+    if a.dtype != np.uint8 or a.ndim != 3 or a.shape[2] != 3:
+        raise SpecError("images must be uint8 HWC arrays with 3 channels")
+    return a
+
+
+def stage_images(images, device="cuda", pinned: bool = True, stream=None) -> ImageBatch:
+    """Concatenate uint8 HWC images (host arrays or tensors) into one device buffer."""
+    imgs = [_as_hwc_u8(i) for i in images]
+    dims = [(int(i.shape[1]), int(i.shape[0])) for i in imgs]
+    for w, h in dims:
+        if w < 1 or h < 1:
+            raise SpecError("image dimensions must be >= 1 pixel")
+    sizes = [w * h * 3 for w, h in dims]
+    offs = np.zeros(len(imgs), np.int64)
+    if imgs:
+        offs[1:] = np.cumsum(sizes)[:-1]
+    total = int(sum(sizes))
+    dev = torch.device(device)
+    meta = np.concatenate([offs.view(np.int32), np.array([d[0] for d in dims], np.int32),
+                           np.array([d[1] for d in dims], np.int32)]) if imgs else np.zeros(0, np.int32)
+    host = torch.empty(total, dtype=torch.uint8, pin_memory=pinned)
+    hv = host.numpy()
+    for i, im in enumerate(imgs):
+        a = im.cpu().numpy() if isinstance(im, torch.Tensor) else im
+        hv[offs[i]:offs[i] + sizes[i]] = a.reshape(-1)
+    hmeta = torch.from_numpy(meta)
+    if pinned:
+        hmeta = hmeta.pin_memory()
+    src = host.to(dev, non_blocking=True)
+    dmeta = hmeta.to(dev, non_blocking=True)
+    n = len(imgs)
+    src_off = dmeta[:2 * n].view(torch.int64)
+    return ImageBatch(src=src, src_off=src_off, w=dmeta[2 * n:3 * n], h=dmeta[3 * n:4 * n], dims=dims,
+                      h2d_bytes=total + meta.nbytes)
+
+
+class ImagePathExecutor:
+    """preprocess -> encode -> pack for one model on one GPU (one process per GPU)."""
+
+    def __init__(self, spec: ModelSpec, weights: dict | None = None, seed: int = 0, device="cuda"):
+        if spec.encoder is None:
+            from ._lib import ProfileError
+            raise ProfileError(f"{spec.name}: no encoder configuration; the image path needs one")
+        self.spec = spec
+        self.device = torch.device(device)
+        self.weights = weights if weights is not None else init_weights(spec, seed)
+        self.encoder = DeviceEncoder(spec, self.weights, self.device)
+
+    # ------------------------------------------------------------------ core path
+    def encode(self, batch: ImageBatch) -> PackedBatch:
+        spec, enc = self.spec, self.spec.encoder
+        n = batch.n
+        if n == 0:
+            raise SpecError("encode batch must contain at least one image")
+        tiles = [tile_count(w, h, spec) for w, h in batch.dims]
+        total_tiles = sum(tiles)
+        P = (spec.tile_edge_px // enc.patch_px) ** 2
+        plan = ops.tile_plan(batch.w, batch.h, spec)
+        patches = ops.preprocess(batch.src, batch.src_off, batch.w, batch.h, plan["tile_off"], plan["geom"], n,
+                                 total_tiles, spec, self.encoder.k_pad, self.encoder.norm_scale,
+                                 self.encoder.norm_shift)
+        # attention sequences: all tokens of one image (images never attend to each other)
+        seq = np.zeros(n + 1, np.int32)
+        seq[1:] = np.cumsum(np.asarray(tiles, np.int64) * (P + 1))
+        cu = torch.from_numpy(seq).pin_memory().to(self.device, non_blocking=True)
+        max_s = int(max(tiles)) * (P + 1)
+        if enc.family == "mllama":
+            tile_image, tile_slot = ops.tile_index(plan["tile_off"], n, total_tiles)
+            emb = self.encoder.forward(patches, total_tiles, cu, n, max_s, tile_image, tile_slot, plan["ar_id"])
+        else:
+            emb = self.encoder.forward(patches, total_tiles, cu, n, max_s)
+        return PackedBatch(embeds=emb, tok_offsets=plan["tok_off"], tiles=tiles,
+                           image_tokens=[t * spec.tokens_per_tile for t in tiles])
+
+    def encode_images(self, images, pinned: bool = True) -> PackedBatch:
+        return self.encode(stage_images(images, self.device, pinned))
+
+    # ------------------------------------------------------------------ batcher API
+    def run(self, batch: list[WorkItem], images: dict) -> PackedBatch:
+        """Execute one ``form_batch`` result of ENCODE (or PREPROCESS) items.
+
+        images: request_id -> list of uint8 HWC images of that request; each item's
+        ``shard_images`` selects its images (reference engine.py:604-625)."""
+        if not batch:
+            raise SpecError("empty batch")
+        flat, spans = [], {}
+        for it in batch:
+            if it.stage not in (StageKind.ENCODE, StageKind.PREPROCESS):
+                raise SpecError(f"item {it.seq}: stage {it.stage.value} is not on the image path")
+            req_imgs = images[it.request_id]
+            idx = it.shard_images if it.shard_images else tuple(range(len(req_imgs)))
+            start = len(flat)
+            flat.extend(req_imgs[i] for i in idx)
+            spans[it.seq] = (start, len(flat))
+        out = self.encode_images(flat)
+        out.item_spans = spans
+        return out

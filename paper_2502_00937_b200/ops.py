@@ -1,0 +1,151 @@
+"""Torch-tensor wrappers over the libmmk C ABI (device memory from the PyTorch caching
+allocator, the current CUDA stream, raw pointers across the boundary).  No compute happens in
+Python; every function launches exactly one libmmk kernel (GEMM: one persistent launch)."""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .core import SpecError
+
+EPI_BF16, EPI_BF16_GELU, EPI_BF16_QUICKGELU, EPI_F32, EPI_RESID_F32 = range(5)
+ACT_EPI = {"gelu": EPI_BF16_GELU, "quick_gelu": EPI_BF16_QUICKGELU}
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def _s():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _need(t, dtype, name):
+    if t.dtype != dtype or not t.is_cuda:
+        raise SpecError(f"{name}: expected CUDA {dtype}, got {t.dtype} on {t.device}")
+    if not t.is_contiguous():
+        raise SpecError(f"{name}: expected a contiguous tensor")
+
+
+def tile_plan(w: torch.Tensor, h: torch.Tensor, spec, resize_mode: int | None = None):
+    """K0 on device: dict(tiles, tile_off, tok_off, geom, ar_id, bad) (all device tensors)."""
+    _need(w, torch.int32, "w")
+    _need(h, torch.int32, "h")
+    n = w.numel()
+    dev = w.device
+    tiles = torch.empty(n, dtype=torch.int32, device=dev)
+    tile_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    tok_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    geom = torch.empty(n, 4, dtype=torch.int32, device=dev)
+    ar_id = torch.empty(n, dtype=torch.int32, device=dev)
+    bad = torch.empty(1, dtype=torch.int32, device=dev)
+    if resize_mode is None:
+        resize_mode = spec.encoder.resize_mode if spec.encoder is not None else 0
+    _lib.check(_lib.lib.mmk_tile_plan(w.data_ptr(), h.data_ptr(), n, spec.tile_edge_px, spec.tokens_per_tile,
+                                      spec.max_tiles_per_image, int(spec.thumbnail_tile), resize_mode,
+                                      tiles.data_ptr(), tile_off.data_ptr(), tok_off.data_ptr(), geom.data_ptr(),
+                                      ar_id.data_ptr(), bad.data_ptr(), _s()))
+    return {"tiles": tiles, "tile_off": tile_off, "tok_off": tok_off, "geom": geom, "ar_id": ar_id, "bad": bad}
+
+
+def tile_index(tile_off: torch.Tensor, n: int, total_tiles: int):
+    tile_image = torch.empty(total_tiles, dtype=torch.int32, device=tile_off.device)
+    tile_slot = torch.empty(total_tiles, dtype=torch.int32, device=tile_off.device)
+    _lib.check(_lib.lib.mmk_tile_index(tile_off.data_ptr(), n, tile_image.data_ptr(), tile_slot.data_ptr(), _s()))
+    return tile_image, tile_slot
+
+
+def preprocess(src, src_off, w, h, tile_off, geom, n: int, total_tiles: int, spec, k_pad: int,
+               scale3: torch.Tensor, shift3: torch.Tensor, out: torch.Tensor | None = None):
+    """K1: uint8 images -> bf16 patch matrix [total_tiles * P, k_pad]."""
+    enc = spec.encoder
+    P = (spec.tile_edge_px // enc.patch_px) ** 2
+    if out is None:
+        out = torch.empty(total_tiles * P, k_pad, dtype=torch.bfloat16, device=src.device)
+    _lib.check(_lib.lib.mmk_preprocess(src.data_ptr(), src_off.data_ptr(), w.data_ptr(), h.data_ptr(),
+                                       tile_off.data_ptr(), geom.data_ptr(), n, total_tiles, spec.tile_edge_px,
+                                       enc.patch_px, k_pad, enc.resize_mode, int(spec.thumbnail_tile),
+                                       scale3.data_ptr(), shift3.data_ptr(), out.data_ptr(), _s()))
+    return out
+
+
+def gemm(a: torch.Tensor, b: torch.Tensor, epilogue: int = EPI_BF16, bias=None, out=None, gate: float = 1.0,
+         aux=None):
+    """out = epilogue(a @ b.T): a [M, K] bf16, b [N, K] bf16 (nn.Linear weight layout)."""
+    m, k = a.shape
+    n = b.shape[0]
+    if b.shape[1] != k:
+        raise SpecError(f"gemm: K mismatch {a.shape} x {b.shape}")
+    f32_out = epilogue in (EPI_F32, EPI_RESID_F32)
+    if out is None:
+        if epilogue == EPI_RESID_F32:
+            raise SpecError("gemm: RESID_F32 needs the residual tensor as `out`")
+        out = torch.empty(m, n, dtype=torch.float32 if f32_out else torch.bfloat16, device=a.device)
+    _lib.check(_lib.lib.mmk_gemm_bf16(a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), m, n, k, epilogue,
+                                      _p(bias), out.data_ptr(), out.stride(0), float(gate), _p(aux),
+                                      aux.stride(0) if aux is not None else 0, _s()))
+    return out
+
+
+def layernorm(x, gamma, beta, eps: float, out=None, out_f32: bool = False, tile_add=None, tile_image=None,
+              image_table=None, tile_slot=None, rows_per_tile: int = 0, slots: int = 0):
+    rows, d = x.shape
+    if out is None:
+        out = torch.empty(rows, d, dtype=torch.float32 if out_f32 else torch.bfloat16, device=x.device)
+    _lib.check(_lib.lib.mmk_layernorm(x.data_ptr(), out.data_ptr(), int(out_f32), rows, d, gamma.data_ptr(),
+                                      beta.data_ptr(), float(eps), _p(tile_add), _p(tile_image), _p(image_table),
+                                      _p(tile_slot), rows_per_tile, slots, _s()))
+    return out
+
+
+def attention(qkv, cu_seqlens, n_seq: int, max_seqlen: int, heads: int, head_dim: int, out=None,
+              scale: float | None = None):
+    T = qkv.shape[0]
+    if out is None:
+        out = torch.empty(T, heads * head_dim, dtype=torch.bfloat16, device=qkv.device)
+    if scale is None:
+        scale = head_dim ** -0.5
+    _lib.check(_lib.lib.mmk_attention_varlen_bf16(qkv.data_ptr(), out.data_ptr(), cu_seqlens.data_ptr(), n_seq,
+                                                  max_seqlen, heads, head_dim, float(scale), _s()))
+    return out
+
+
+def embed_tokens(patch_out, total_tiles: int, patches_per_tile: int, cls, pos, pos_scale: float, gamma, beta,
+                 eps: float, tile_image=None, tile_slot=None, image_ar=None, tile_pos=None,
+                 tile_pos_scale: float = 0.0, pre_tile=None, pre_scale: float = 0.0, slots: int = 0, out=None):
+    d = patch_out.shape[1]
+    rows = total_tiles * (patches_per_tile + 1)
+    if out is None:
+        out = torch.empty(rows, d, dtype=torch.float32, device=patch_out.device)
+    _lib.check(_lib.lib.mmk_embed_tokens(patch_out.data_ptr(), _p(tile_image), _p(tile_slot), _p(image_ar),
+                                         total_tiles, patches_per_tile, d, cls.data_ptr(), pos.data_ptr(),
+                                         float(pos_scale), _p(tile_pos), float(tile_pos_scale), _p(pre_tile),
+                                         float(pre_scale), slots, gamma.data_ptr(), beta.data_ptr(), float(eps),
+                                         out.data_ptr(), _s()))
+    return out
+
+
+def pack_mllama(final_resid, inter, out=None):
+    rows, d = final_resid.shape
+    n_inter = inter.shape[0] if inter is not None else 0
+    if out is None:
+        out = torch.empty(rows, d * (1 + n_inter), dtype=torch.bfloat16, device=final_resid.device)
+    _lib.check(_lib.lib.mmk_pack_mllama(final_resid.data_ptr(), _p(inter), n_inter, rows, d, out.data_ptr(), _s()))
+    return out
+
+
+def pack_drop_cls(src, tiles: int, tokens_per_tile: int, drop: int, out=None):
+    d = src.shape[1]
+    if out is None:
+        out = torch.empty(tiles * (tokens_per_tile - drop), d, dtype=torch.bfloat16, device=src.device)
+    _lib.check(_lib.lib.mmk_pack_drop_cls(src.data_ptr(), int(src.dtype == torch.float32), tiles, tokens_per_tile,
+                                          drop, d, out.data_ptr(), _s()))
+    return out
+
+
+def checksum(x, out=None):
+    if out is None:
+        out = torch.empty(1, dtype=torch.float32, device=x.device)
+    _lib.check(_lib.lib.mmk_checksum_bf16(x.data_ptr(), x.numel(), out.data_ptr(), _s()))
+    return out

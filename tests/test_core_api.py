@@ -1,0 +1,126 @@
+"""Unit tests of the host-side stage API, mirroring the reference's own test strategy
+(/root/reference/pkg/tests/test_core.py, test_policies.py:173-186, test_engine.py:174-253)."""
+
+import json
+
+import pytest
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+from paper_2502_00937_b200 import batcher, core, policies
+from paper_2502_00937_b200.core import SpecError, StageKind
+
+LLAMA = core.get_model_spec("llama3.2-11b")
+INTERNVL = core.get_model_spec("internvl-26b")
+LLAVA = core.get_model_spec("llava-ov-7b")
+
+
+def test_known_token_counts():  # reference test_core.py:27-38
+    assert core.image_tokens(896, 896, LLAMA) == 6404
+    assert core.image_tokens(896, 896, INTERNVL) == 1280
+    assert core.image_tokens(896, 896, LLAVA) == 7290
+    for spec in (LLAMA, INTERNVL, LLAVA):
+        assert core.image_tokens(1, 1, spec) == spec.tokens_per_tile
+
+
+def test_degenerate_dims_rejected():
+    with pytest.raises(SpecError):
+        core.image_tokens(0, 10, LLAMA)
+    with pytest.raises(SpecError):
+        core.tile_count(10, -1, LLAMA)
+
+
+@given(w=st.integers(1, 4000), h=st.integers(1, 4000), dw=st.integers(0, 500))
+@settings(max_examples=200, deadline=None)
+def test_monotone_in_width(w, h, dw):
+    assert core.image_tokens(w + dw, h, INTERNVL) >= core.image_tokens(w, h, INTERNVL)
+
+
+@given(w=st.integers(1, 8000), h=st.integers(1, 8000))
+@settings(max_examples=200, deadline=None)
+def test_tile_cap(w, h):
+    for spec in (LLAMA, INTERNVL, LLAVA):
+        assert 1 <= core.tile_count(w, h, spec) <= spec.max_tiles_per_image
+
+
+def test_thumbnail_only_above_one_tile():
+    assert core.tile_count(448, 448, INTERNVL) == 1
+    assert core.tile_count(896, 448, INTERNVL) == 3
+
+
+def test_request_totals():
+    img = core.ImageSpec.from_dims(896, 896, INTERNVL)
+    r = core.Request(id=0, arrival_ms=0, text_tokens=5, images=(img, img), output_tokens=1)
+    assert core.request_totals(r) == (5, 2560, 2565)
+    assert r.total_tiles == 10 and r.is_multimodal
+    with pytest.raises(SpecError):
+        core.Request(id=0, arrival_ms=0, text_tokens=-1, images=(), output_tokens=1)
+    with pytest.raises(SpecError):
+        core.Request(id=0, arrival_ms=0, text_tokens=0, images=(), output_tokens=0)
+
+
+def test_presets_and_user_spec(tmp_path):
+    specs = core.load_model_specs()
+    for name in ("llama3.2-11b", "llama3.2-90b", "llava-ov-7b", "llava-ov-72b", "internvl-26b", "nvlm-d-72b"):
+        assert name in specs
+    assert specs["llama3.2-11b"].encoder.family == "mllama"
+    assert specs["llama3.2-11b"].encoder.head_dim == 80
+    assert specs["llava-clip-l14-336"].encoder.head_dim == 64
+    with pytest.raises(SpecError):
+        core.get_model_spec("gpt-oss-999t")
+    path = tmp_path / "m.json"
+    path.write_text(json.dumps([{"name": "toy", "architecture": "dec_only", "tile_edge_px": 100,
+                                 "tokens_per_tile": 10, "max_tiles_per_image": 3}]))
+    toy = core.load_model_specs(path)["toy"]
+    assert core.image_tokens(250, 50, toy) == 30
+    path.write_text(json.dumps([{"name": "bad", "architecture": "dec_only", "tile_edge_px": 0,
+                                 "tokens_per_tile": 10, "max_tiles_per_image": 3}]))
+    with pytest.raises(SpecError):
+        core.load_model_specs(path)
+    # encoder token count must agree with tokens_per_tile
+    path.write_text(json.dumps([{"name": "e", "architecture": "dec_only", "tile_edge_px": 224,
+                                 "tokens_per_tile": 100, "max_tiles_per_image": 1,
+                                 "encoder": {"family": "clip", "patch_px": 16, "hidden": 768, "ffn": 3072,
+                                             "layers": 1, "heads": 12}}]))
+    with pytest.raises(SpecError):
+        core.load_model_specs(path)
+
+
+def test_split_by_tiles_balance():  # reference test_policies.py:173-186
+    tiles = [5, 4, 3, 3, 1]
+    assert sorted(sum(tiles[i] for i in s) for s in policies.split_by_tiles(tiles, 2)) == [8, 8]
+
+
+@given(st.lists(st.integers(1, 10), min_size=1, max_size=16), st.integers(1, 8))
+@settings(max_examples=200, deadline=None)
+def test_partition_is_complete(tiles, n):
+    shards = policies.split_by_tiles(tiles, n)
+    assert sorted(i for s in shards for i in s) == list(range(len(tiles)))
+    shards = policies.split_by_cost([float(t) ** 1.5 for t in tiles], n)
+    assert sorted(i for s in shards for i in s) == list(range(len(tiles)))
+
+
+def test_encode_shard():  # reference test_engine.py:174-191
+    imgs = [core.ImageSpec.from_dims(448, 448, INTERNVL), core.ImageSpec.from_dims(896, 896, INTERNVL),
+            core.ImageSpec.from_dims(448, 448, INTERNVL), core.ImageSpec.from_dims(448, 448, INTERNVL)]
+    shards = batcher.encode_shard(imgs, 2)
+    loads = [sum(imgs[i].tiles for i in s) for s in shards]
+    assert max(loads) - min(loads) <= 2
+    assert batcher.encode_shard(imgs[:1], 4) == [[0]]
+    assert batcher.encode_shard([], 4) == []
+
+
+def _item(seq, stage, size=10, enqueue=0.0, deps=()):
+    return batcher.WorkItem(seq=seq, request_id=seq, stage=stage, size_tokens=size, tiles=1, enqueue_ms=enqueue,
+                            ttft_slo_ms=1000.0, deps=set(deps))
+
+
+def test_form_batch_rules():  # reference test_engine.py:226-253
+    q = [_item(i, StageKind.ENCODE, enqueue=i) for i in range(5)]
+    assert batcher.form_batch(q, 10.0, policies.SchedulerKind.FIFO, 0.5, {"encode": 2}) == [0, 1]
+    q = [_item(0, StageKind.ENCODE), _item(1, StageKind.PREFILL), _item(2, StageKind.ENCODE)]
+    picked = batcher.form_batch(q, 10.0, policies.SchedulerKind.FIFO, 0.5, {"encode": 4, "prefill": 4})
+    assert all(q[i].stage is StageKind.ENCODE for i in picked)
+    q = [_item(0, StageKind.ENCODE, deps={99}), _item(1, StageKind.ENCODE)]
+    assert batcher.form_batch(q, 10.0, policies.SchedulerKind.FIFO, 0.5, {"encode": 2}) == [1]
+    assert batcher.form_batch([], 0.0, policies.SchedulerKind.FIFO, 0.5, {}) == []

@@ -1,0 +1,82 @@
+"""End-to-end image path on a B200 vs the fp32 CPU oracle (uint8 pixels -> packed embeddings).
+
+Tolerance (north_star): norm-wise relative error ||y - y_ref|| / ||y_ref|| <= 1e-2 per image for
+the bf16 path against the fp32 oracle; preprocessing is bit-exact (checked separately).
+Reduced-depth encoders keep the CPU oracle fast; one full-depth Mllama image runs too.
+"""
+
+import dataclasses
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import encoders as oenc  # noqa: E402
+from oracle import preprocess as oprep  # noqa: E402
+from oracle import tiling as otiling  # noqa: E402
+
+REL_TOL = 1e-2
+
+
+def _reduced(spec, layers, global_layers=None, out_layers=None):
+    enc = spec.encoder
+    kw = {"layers": layers}
+    if global_layers is not None:
+        kw["global_layers"] = global_layers
+    if out_layers is not None:
+        kw["out_layers"] = tuple(out_layers)
+    return dataclasses.replace(spec, encoder=dataclasses.replace(enc, **kw))
+
+
+def _run(spec, dims, seed=0):
+    from paper_2502_00937_b200.encoders import k_pad_of
+    from paper_2502_00937_b200.executor import ImagePathExecutor
+    rng = np.random.default_rng(seed)
+    imgs = [rng.integers(0, 256, (h, w, 3), dtype=np.uint8) for w, h in dims]
+    ex = ImagePathExecutor(spec, seed=seed)
+    out = ex.encode_images(imgs)
+    torch.cuda.synchronize()
+    enc = spec.encoder
+    oplan = otiling.tile_plan([d[0] for d in dims], [d[1] for d in dims], spec.tile_edge_px, spec.tokens_per_tile,
+                              spec.max_tiles_per_image, spec.thumbnail_tile, enc.resize_mode)
+    scale, shift = oprep.norm_constants(enc.mean, enc.std)
+    patches = oprep.bf16_bits_to_f32(oprep.preprocess(imgs, oplan, spec.tile_edge_px, enc.patch_px, k_pad_of(spec),
+                                                      enc.resize_mode, spec.thumbnail_tile, scale, shift))
+    ref = oenc.encode(torch.from_numpy(patches), oplan, ex.weights, spec)
+    got = out.embeds.float().cpu()
+    assert got.shape == ref.shape, (got.shape, ref.shape)
+    assert out.tok_offsets.cpu().tolist() == oplan["tok_off"].tolist()
+    offs = oplan["tok_off"]
+    worst = 0.0
+    for i in range(len(dims)):
+        a, b = int(offs[i]), int(offs[i + 1])
+        rel = ((got[a:b] - ref[a:b]).norm() / ref[a:b].norm()).item()
+        worst = max(worst, rel)
+    assert worst <= REL_TOL, f"worst per-image rel err {worst:.3g}"
+    return worst
+
+
+def test_mllama_reduced_depth():
+    from paper_2502_00937_b200 import core
+    spec = _reduced(core.get_model_spec("llama3.2-11b"), layers=4, global_layers=2, out_layers=[1, 2, 3, 4])
+    _run(spec, [(560, 560), (1000, 500), (1500, 1200), (300, 2000), (1120, 1120)])
+
+
+def test_mllama_full_depth_one_image():
+    from paper_2502_00937_b200 import core
+    spec = core.get_model_spec("llama3.2-11b")
+    _run(spec, [(900, 500)], seed=1)
+
+
+def test_clip_l336_llava_penultimate():
+    from paper_2502_00937_b200 import core
+    spec = _reduced(core.get_model_spec("llava-clip-l14-336"), layers=4)
+    _run(spec, [(336, 336), (640, 480), (480, 640), (1000, 200)])
+
+
+def test_vit_b16_batch8():
+    from paper_2502_00937_b200 import core
+    spec = core.get_model_spec("vit-b16-224")
+    _run(spec, [(224, 224)] * 8, seed=2)

@@ -1,0 +1,242 @@
+"""Parity of each libmmk kernel on a B200 against its checker:
+  K0 tile plan     -> oracle/tile_plan.c (bit-exact), itself pinned to reference golden vectors
+  K1 preprocess    -> oracle/preprocess.py (bit-exact bf16)
+  GEMM epilogues   -> torch fp32 reference of the same op (tolerance below)
+  K5 attention     -> torch fp32 softmax attention per sequence
+  K3 / embed / K9  -> torch fp32
+"""
+
+import json
+import math
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import preprocess as oprep  # noqa: E402
+from oracle import tiling as otiling  # noqa: E402
+
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+@pytest.fixture(scope="module")
+def mk():
+    from paper_2502_00937_b200 import core, encoders, ops
+    return core, ops, encoders
+
+
+def _plan_dev(ops, spec, w, h, mode):
+    wd = torch.tensor(w, dtype=torch.int32, device="cuda")
+    hd = torch.tensor(h, dtype=torch.int32, device="cuda")
+    return ops.tile_plan(wd, hd, spec, resize_mode=mode)
+
+
+# ----------------------------------------------------------------------------- K0
+def test_tile_plan_bit_exact_vs_oracle_on_reference_golden(mk):
+    core, ops, _ = mk
+    gold = json.loads((GOLD / "tiling.json").read_text())
+    for name, entry in gold.items():
+        T, tok, cap, thumb = entry["spec"]
+        spec = core.ModelSpec(name=name, architecture=core.Architecture.DEC_ONLY, tile_edge_px=T,
+                              tokens_per_tile=tok, max_tiles_per_image=cap, thumbnail_tile=bool(thumb))
+        rows = [r for r in entry["rows"] if abs(r[0]) < 2**31 and abs(r[1]) < 2**31]
+        w = [r[0] for r in rows]
+        h = [r[1] for r in rows]
+        for mode in (0, 1):
+            dev = _plan_dev(ops, spec, w, h, mode)
+            ref = otiling.tile_plan(w, h, T, tok, cap, bool(thumb), mode)
+            np.testing.assert_array_equal(dev["tiles"].cpu().numpy(), ref["tiles"])
+            np.testing.assert_array_equal(dev["tile_off"].cpu().numpy(), ref["tile_off"])
+            np.testing.assert_array_equal(dev["tok_off"].cpu().numpy(), ref["tok_off"])
+            np.testing.assert_array_equal(dev["geom"].cpu().numpy(), ref["geom"])
+            assert int(dev["bad"].item()) == ref["bad"]
+            # reference values themselves
+            np.testing.assert_array_equal(dev["tiles"].cpu().numpy(), [max(r[2], 0) for r in rows])
+
+
+def test_tile_plan_max_batch_and_empty(mk):
+    core, ops, _ = mk
+    spec = core.get_model_spec("llama3.2-11b")
+    rng = np.random.default_rng(5)
+    w = rng.integers(1, 20000, 65536).tolist()
+    h = rng.integers(1, 20000, 65536).tolist()
+    dev = _plan_dev(ops, spec, w, h, 0)
+    ref = otiling.tile_plan(w, h, 560, 1601, 4, False, 0)
+    np.testing.assert_array_equal(dev["tok_off"].cpu().numpy(), ref["tok_off"])
+    np.testing.assert_array_equal(dev["geom"].cpu().numpy(), ref["geom"])
+    # aspect-ratio ids: transformers' supported_aspect_ratios order
+    from oracle.encoders import aspect_ratio_id
+    g = ref["geom"][:2000]
+    np.testing.assert_array_equal(dev["ar_id"].cpu().numpy()[:2000], [aspect_ratio_id(r, c) for r, c, _, _ in g])
+    empty = _plan_dev(ops, spec, [], [], 0)
+    assert empty["tile_off"].cpu().tolist() == [0]
+    from paper_2502_00937_b200.core import SpecError
+    with pytest.raises(SpecError):
+        _plan_dev(ops, spec, [1] * 65537, [1] * 65537, 0)
+
+
+# ----------------------------------------------------------------------------- K1
+def _rand_images(dims, seed):
+    rng = np.random.default_rng(seed)
+    return [rng.integers(0, 256, (h, w, 3), dtype=np.uint8) for w, h in dims]
+
+
+def _check_preprocess(core, ops, encoders, spec, dims, seed=0):
+    from paper_2502_00937_b200.executor import stage_images
+    imgs = _rand_images(dims, seed)
+    b = stage_images(imgs)
+    enc = spec.encoder
+    tiles = [core.tile_count(w, h, spec) for w, h in dims]
+    plan = ops.tile_plan(b.w, b.h, spec)
+    k_pad = encoders.k_pad_of(spec)
+    scale, shift = oprep.norm_constants(enc.mean, enc.std)
+    out = ops.preprocess(b.src, b.src_off, b.w, b.h, plan["tile_off"], plan["geom"], len(dims), sum(tiles), spec,
+                         k_pad, torch.from_numpy(scale).cuda(), torch.from_numpy(shift).cuda())
+    oplan = otiling.tile_plan([d[0] for d in dims], [d[1] for d in dims], spec.tile_edge_px, spec.tokens_per_tile,
+                              spec.max_tiles_per_image, spec.thumbnail_tile, enc.resize_mode)
+    ref = oprep.preprocess(imgs, oplan, spec.tile_edge_px, enc.patch_px, k_pad, enc.resize_mode,
+                           spec.thumbnail_tile, scale, shift)
+    got = out.view(torch.int16).cpu().numpy().view(np.uint16)
+    mism = int((got != ref).sum())
+    assert mism == 0, f"{mism} of {ref.size} bf16 values differ"
+
+
+def test_preprocess_mllama_bit_exact(mk):
+    core, ops, encoders = mk
+    spec = core.get_model_spec("llama3.2-11b")
+    dims = [(560, 560), (1000, 500), (1120, 1120), (1700, 600), (333, 901), (64, 64), (4096, 300), (1, 1),
+            (561, 559), (2300, 2300)]
+    _check_preprocess(core, ops, encoders, spec, dims)
+
+
+def test_preprocess_clip_bit_exact(mk):
+    core, ops, encoders = mk
+    for name in ("vit-b16-224", "llava-clip-l14-336"):
+        spec = core.get_model_spec(name)
+        dims = [(224, 224), (336, 336), (500, 375), (375, 500), (64, 900), (1024, 1024), (337, 336)]
+        _check_preprocess(core, ops, encoders, spec, dims, seed=3)
+
+
+def test_preprocess_thumbnail_spec_bit_exact(mk):
+    core, ops, encoders = mk
+    enc = core.EncoderSpec(family="clip", patch_px=14, hidden=128, ffn=256, layers=1, heads=2, resize_mode=0)
+    spec = core.ModelSpec(name="thumb", architecture=core.Architecture.DEC_ONLY, tile_edge_px=448,
+                          tokens_per_tile=1025, max_tiles_per_image=5, thumbnail_tile=True, encoder=enc)
+    dims = [(448, 448), (896, 448), (1500, 1500), (3000, 500), (200, 100)]
+    _check_preprocess(core, ops, encoders, spec, dims, seed=9)
+
+
+# ----------------------------------------------------------------------------- GEMM
+@pytest.mark.parametrize("m,n,k", [(1, 256, 64), (129, 768, 592), (1576, 2304, 768), (5000, 3840, 1280),
+                                   (3000, 1280, 5120), (700, 1024, 4096)])
+@pytest.mark.parametrize("epi", [0, 1, 2, 3, 4])
+def test_gemm_epilogues(mk, m, n, k, epi):
+    _, ops, _ = mk
+    g = torch.Generator(device="cuda").manual_seed(m * 7 + n + epi)
+    a = torch.randn(m, k, device="cuda", generator=g).bfloat16()
+    b = (torch.randn(n, k, device="cuda", generator=g) * 0.05).bfloat16()
+    bias = torch.randn(n, device="cuda", generator=g)
+    ref = a.float() @ b.float().t() + bias
+    if epi == 1:
+        ref = torch.nn.functional.gelu(ref)
+    elif epi == 2:
+        ref = ref * torch.sigmoid(1.702 * ref)
+    if epi == 4:
+        base = torch.randn(m, n, device="cuda", generator=g)
+        out = base.clone()
+        aux = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+        ops.gemm(a, b, 4, bias=bias, out=out, gate=-0.7, aux=aux)
+        ref = base - 0.7 * ref
+        torch.testing.assert_close(out, ref, rtol=1e-4, atol=1e-3)
+        torch.testing.assert_close(aux.float(), ref, rtol=1e-2, atol=1e-2)
+        return
+    out = ops.gemm(a, b, epi, bias=bias)
+    tol = dict(rtol=1e-4, atol=1e-3) if epi == 3 else dict(rtol=1e-2, atol=2e-2)
+    torch.testing.assert_close(out.float(), ref, **tol)
+
+
+def test_gemm_strided_operands(mk):
+    _, ops, _ = mk
+    a_full = torch.randn(300, 1024, device="cuda").bfloat16()
+    a = a_full[:, :512]
+    b = torch.randn(256, 512, device="cuda").bfloat16()
+    out = torch.zeros(300, 768, device="cuda", dtype=torch.bfloat16)
+    ops.gemm(a, b, 0, out=out[:, 256:512])
+    torch.testing.assert_close(out[:, 256:512].float(), a.float() @ b.float().t(), rtol=1e-2, atol=5e-2)
+    assert out[:, :256].abs().sum().item() == 0 and out[:, 512:].abs().sum().item() == 0
+
+
+# ----------------------------------------------------------------------------- attention
+def _attn_ref(qkv, lens, heads, hd):
+    outs = []
+    d = heads * hd
+    start = 0
+    for L in lens:
+        x = qkv[start:start + L].float()
+        q, k, v = x[:, :d], x[:, d:2 * d], x[:, 2 * d:]
+        q = q.view(L, heads, hd).transpose(0, 1)
+        k = k.view(L, heads, hd).transpose(0, 1)
+        v = v.view(L, heads, hd).transpose(0, 1)
+        s = (q @ k.transpose(1, 2)) * hd ** -0.5
+        o = torch.softmax(s, -1) @ v
+        outs.append(o.transpose(0, 1).reshape(L, d))
+        start += L
+    return torch.cat(outs)
+
+
+@pytest.mark.parametrize("hd,heads,lens", [(80, 16, [1601, 3202, 1, 63, 64, 65, 6404]),
+                                           (64, 16, [577, 577, 129]), (64, 12, [197] * 8), (80, 4, [17, 4803])])
+def test_attention_varlen(mk, hd, heads, lens):
+    _, ops, _ = mk
+    T = sum(lens)
+    qkv = torch.randn(T, 3 * heads * hd, device="cuda").bfloat16()
+    cu = torch.tensor(np.concatenate([[0], np.cumsum(lens)]), dtype=torch.int32, device="cuda")
+    out = ops.attention(qkv, cu, len(lens), max(lens), heads, hd)
+    ref = _attn_ref(qkv, lens, heads, hd)
+    err = (out.float() - ref).abs().max().item()
+    assert err < 2e-2, err
+
+
+# ----------------------------------------------------------------------------- norms / embed / pack
+def test_layernorm_and_tile_add(mk):
+    _, ops, _ = mk
+    for d in (768, 1024, 1280):
+        x = torch.randn(1000, d, device="cuda") * 3 + 1
+        gw, gb = torch.randn(d, device="cuda"), torch.randn(d, device="cuda")
+        y = ops.layernorm(x, gw, gb, 1e-5)
+        ref = torch.nn.functional.layer_norm(x, (d,), gw, gb, 1e-5)
+        torch.testing.assert_close(y.float(), ref, rtol=1e-2, atol=2e-2)
+    d, rpt = 1280, 10
+    x = torch.randn(7 * rpt, d, device="cuda")
+    table = torch.randn(9, 4, d, device="cuda")
+    tile_image = torch.tensor([0, 0, 1, 2, 2, 2, 2], dtype=torch.int32, device="cuda")
+    tile_slot = torch.tensor([0, 1, 0, 0, 1, 2, 3], dtype=torch.int32, device="cuda")
+    img_ar = torch.tensor([2, 1, 6], dtype=torch.int32, device="cuda")
+    y = ops.layernorm(x.clone(), gw, gb, 1e-5, out_f32=True, tile_add=table, tile_image=tile_image,
+                      image_table=img_ar, tile_slot=tile_slot, rows_per_tile=rpt, slots=4)
+    ref = torch.nn.functional.layer_norm(x, (d,), gw, gb, 1e-5)
+    idx = img_ar[tile_image.long()].long()
+    ref = ref + table[idx, tile_slot.long()].repeat_interleave(rpt, 0)
+    torch.testing.assert_close(y, ref, rtol=1e-4, atol=1e-4)
+
+
+def test_pack_mllama_layout(mk):
+    _, ops, _ = mk
+    rows, d, n_inter = 333, 1280, 5
+    fin = torch.randn(rows, d, device="cuda")
+    inter = torch.randn(n_inter, rows, d, device="cuda").bfloat16()
+    out = ops.pack_mllama(fin, inter)
+    ref = torch.cat([fin.bfloat16(), torch.stack(list(inter), dim=-1).reshape(rows, -1)], -1)
+    assert torch.equal(out, ref)
+
+
+def test_pack_drop_cls(mk):
+    _, ops, _ = mk
+    src = torch.randn(4 * 577, 1024, device="cuda")
+    out = ops.pack_drop_cls(src, 4, 577, 1)
+    assert torch.equal(out, src.view(4, 577, 1024)[:, 1:].reshape(-1, 1024).bfloat16())
+    srcb = src.bfloat16()
+    assert torch.equal(ops.pack_drop_cls(srcb, 4, 577, 0), srcb)
