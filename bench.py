@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""Image-path benchmark (preprocess + encode + pack) on 1..N B200s — the driver contract.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mmk|reference] [--model M] [--batch B]
+
+One step = one pass of the image path (K0 tile plan -> K1 preprocess -> encoder K2-K8 -> K9 pack)
+over one batch of B synthetic images per GPU.  Default workload = BASELINE.json configs[1]:
+Llama-3.2-11B-Vision encoder (560 px tiles, <= 4 tiles), image sizes drawn by the reference's
+own workload generator (seed 0), random-init weights, bf16 compute / fp32 accumulate.
+
+Prints ONE JSON line on rank 0.  ``value`` is whole-job images/s with the uint8 images already
+resident in HBM; ``e2e`` is the same metric through the public API
+(ImagePathExecutor.encode_images) from pinned host memory, with H2D of the images and a D2H of
+the token offsets + a checksum of the packed embeddings inside the timed region.  For N > 1 each
+rank encodes its own shard (weak scaling) and hands its packed embeddings to rank 0 (the
+LLM-backend GPU) with NCCL point-to-point sends inside the timed region (BASELINE configs[3]).
+
+``--impl reference`` times the CPU implementation of the path (the oracle port in oracle/:
+numpy preprocess + torch fp32 encoder, all host threads) on a bounded sample per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "llama3.2-11b": dict(config="Llama-3.2-11B-Vision image encoder, 560px tiles (<=4), 1 B200 bf16",
+                         batch=32, generator=dict()),
+    "llava-clip-l14-336": dict(config="LLaVA-style CLIP ViT-L/14-336, layer -2, CLS dropped, ragged packing",
+                               batch=256, generator=dict()),
+    "vit-b16-224": dict(config="reference default: 224x224 single tile -> ViT-B/16", batch=8, fixed=(224, 224)),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mmk", choices=["mmk", "reference"])
+    ap.add_argument("--model", default="llama3.2-11b", choices=sorted(WORKLOADS))
+    ap.add_argument("--batch", type=int, default=0, help="images per GPU per step (0 = workload default)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-images", type=int, default=2)
+    return ap.parse_args()
+
+
+def image_dims(spec, n_images: int, seed: int = 0, fixed=None):
+    """Image sizes from the reference generator (workload.py:247-252), image requests only."""
+    if fixed is not None:
+        return [tuple(fixed)] * n_images
+    from paper_2502_00937_b200 import workload
+    cfg = workload.GeneratorConfig(model=spec, base_rate=50.0, image_request_fraction=1.0, seed=seed)
+    dims = []
+    horizon = 10_000.0
+    while len(dims) < n_images:
+        dims = workload.image_dims_of(workload.generate(cfg, horizon))
+        horizon *= 2
+    return dims[:n_images]
+
+
+def make_images(dims, seed):
+    rng = np.random.default_rng(seed)
+    return [rng.integers(0, 256, (h, w, 3), dtype=np.uint8) for w, h in dims]
+
+
+def encoder_flops(spec, tiles_list):
+    """Algorithmic FLOPs of the encoder per image:
+    F = L*S*(8d^2 + 4*d*ff) + 4*L*S^2*d + n_patch*2*(3p^2)*d, S = attention length of the image."""
+    enc = spec.encoder
+    P = (spec.tile_edge_px // enc.patch_px) ** 2
+    if enc.family == "clip":
+        L = enc.layers if enc.out_layer == -1 else enc.layers + 1 + enc.out_layer
+    else:
+        L = enc.layers + enc.global_layers
+    d, ff = enc.hidden, enc.ffn
+    tot = 0.0
+    for t in tiles_list:
+        S = t * (P + 1)
+        tot += L * S * (8 * d * d + 4 * d * ff) + 4 * L * S * S * d + t * P * 2 * (3 * enc.patch_px ** 2) * d
+    return tot
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling (NVML) during the timed region."""
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+            "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+            "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def result(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("bf16_tflops_sustained", 1398.9), d.get("bf16_tflops", 1646.7), d.get("hbm_gbs", 6548.2), "measured"
+    return 1400.0, 1590.0, 6650.0, "fallback"
+
+
+def committed_traffic():
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return {}
+    return {}
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+def cpu_reference_time(spec, dims, weights, threads: int):
+    """Time the CPU path (oracle port: numpy preprocess + torch fp32 encoder) on the given images."""
+    import torch
+    from oracle import encoders as oenc
+    from oracle import preprocess as oprep
+    from oracle import tiling as otiling
+    from paper_2502_00937_b200.encoders import k_pad_of
+    torch.set_num_threads(threads)
+    enc = spec.encoder
+    imgs = make_images(dims, 123)
+    scale, shift = oprep.norm_constants(enc.mean, enc.std)
+    t0 = time.perf_counter()
+    plan = otiling.tile_plan([d[0] for d in dims], [d[1] for d in dims], spec.tile_edge_px, spec.tokens_per_tile,
+                             spec.max_tiles_per_image, spec.thumbnail_tile, enc.resize_mode)
+    patches = oprep.bf16_bits_to_f32(oprep.preprocess(imgs, plan, spec.tile_edge_px, enc.patch_px, k_pad_of(spec),
+                                                      enc.resize_mode, spec.thumbnail_tile, scale, shift))
+    out = oenc.encode(torch.from_numpy(patches), plan, weights, spec)
+    _ = float(out.float().sum())
+    return time.perf_counter() - t0
+
+
+def run_reference(args, spec, wl, rank, world):
+    """--impl reference: CPU implementation of the path on this box's host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    from paper_2502_00937_b200.encoders import init_weights
+    threads = len(os.sched_getaffinity(0))
+    weights = init_weights(spec, 0)
+    dims = image_dims(spec, max(64, args.steps + args.warmup), fixed=wl.get("fixed"))
+    per_step = 1 if spec.encoder.family == "mllama" else max(1, min(8, wl["batch"]))
+    times, n_img = [], 0
+    for s in range(args.warmup + args.steps):
+        sample = [dims[(s * per_step + j) % len(dims)] for j in range(per_step)]
+        dt = cpu_reference_time(spec, sample, weights, threads)
+        if s >= args.warmup:
+            times.append(dt)
+            n_img += per_step
+    total = sum(times)
+    val = n_img / total
+    line = {
+        "impl": "reference", "metric": "images/sec (preprocess+encode)", "value": round(val, 4), "unit": "images/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1000 * total / len(times), 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": wl["config"], "model": spec.name, "images_per_step": per_step,
+                   "image_dims": "reference generator seed 0"},
+        "cpu_baseline": {"value": round(val, 4), "unit": "images/s", "cores": threads, "kind": "port",
+                         "sample": f"{per_step} image(s)/step from the reference generator dims, "
+                                   f"numpy preprocess + torch fp32 encoder on {threads} threads"},
+        "e2e": {"value": round(val, 4), "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU path
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2502_00937_b200 import core
+    spec = core.get_model_spec(args.model)
+    wl = WORKLOADS[args.model]
+    if args.impl == "reference":
+        return run_reference(args, spec, wl, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2502_00937_b200 import ops
+    from paper_2502_00937_b200.dp import Handoff
+    from paper_2502_00937_b200.executor import ImagePathExecutor, stage_images
+
+    B = args.batch or wl["batch"]
+    # every rank draws its own disjoint images (weak scaling: per-GPU work fixed as N grows)
+    all_dims = image_dims(spec, B * world, fixed=wl.get("fixed"))
+    dims = all_dims[rank * B:(rank + 1) * B]
+    imgs = make_images(dims, 1000 + rank)
+    ex = ImagePathExecutor(spec, seed=0)
+    staged = stage_images(imgs)  # resident uint8 images in HBM (the `value` leg)
+    tiles = [core.tile_count(w, h, spec) for w, h in dims]
+    flops_per_step = encoder_flops(spec, tiles)
+    handoff = Handoff(rank, world) if world > 1 else None
+    # the receiver computes every source's row count itself from the deterministic plan
+    rank_rows = {r: sum(core.tile_count(w, h, spec) for w, h in all_dims[r * B:(r + 1) * B]) * spec.tokens_per_tile
+                 for r in range(world)}
+    stream = torch.cuda.current_stream()
+
+    def step(batch):
+        out = ex.encode(batch)
+        if handoff is not None:
+            handoff.send(out, sizes=rank_rows)
+        return out
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step(staged)
+    barrier()
+    log = ops.LaunchLog(timing=True)
+    ops.LOG = log
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        start.record(stream)
+        for _ in range(args.steps):
+            step(staged)
+        if handoff is not None:
+            handoff.flush()
+        end.record(stream)
+        barrier()
+    ops.LOG = None
+    ms = start.elapsed_time(end)
+    t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * B * args.steps / (ms_max / 1000.0)
+    kernels = log.summary()
+    launches = log.count
+
+    # --------------------------------------------------------------- e2e through the public API
+    pinned_imgs = imgs
+    ck = torch.empty(1, device="cuda")
+    for _ in range(1):
+        o = ex.encode_images(pinned_imgs)
+        ops.checksum(o.embeds, out=ck)
+    barrier()
+    h2d = d2h = 0
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e_start.record(stream)
+    for _ in range(args.steps):
+        b = stage_images(pinned_imgs)
+        o = ex.encode(b)
+        if handoff is not None:
+            handoff.send(o, sizes=rank_rows)
+        ops.checksum(o.embeds, out=ck)
+        offs = o.tok_offsets.to("cpu", non_blocking=True)
+        cks = ck.to("cpu", non_blocking=True)
+        h2d += b.h2d_bytes
+        d2h += offs.numel() * 8 + 4
+    if handoff is not None:
+        handoff.flush()
+    e_end.record(stream)
+    barrier()
+    e_ms = e_start.elapsed_time(e_end)
+    t = torch.tensor([e_ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e_value = world * B * args.steps / (float(t.item()) / 1000.0)
+    assert np.isfinite(float(cks.item()))
+
+    if rank == 0:
+        sus, burst, hbm, src = measured_peaks()
+        g = kernels.get("gemm", {"ms": 0, "work": 0, "launches": 0})
+        a = kernels.get("attention", {"ms": 0, "work": 0, "launches": 0})
+        g_tf = g["work"] / (g["ms"] / 1e3) / 1e12 if g["ms"] else 0.0
+        a_tf = a["work"] / (a["ms"] / 1e3) / 1e12 if a["ms"] else 0.0
+        traffic = committed_traffic()
+        step_ms = ms_max / args.steps
+        enc_tf = flops_per_step / (step_ms / 1e3) / 1e12
+        line = {
+            "metric": "images/sec (preprocess+encode)", "value": round(value, 3), "unit": "images/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (reference generator image sizes, random uint8 pixels, random-init weights)",
+            "config": {"workload": wl["config"], "model": spec.name, "images_per_gpu_per_step": B,
+                       "tiles_per_gpu_per_step": int(sum(tiles)),
+                       "tokens_per_gpu_per_step": int(sum(tiles)) * spec.tokens_per_tile,
+                       "l2": "inputs > L2 (activations of one step are several GB)",
+                       "parallelism": f"dp{world}" + ("+p2p-handoff-to-rank0" if world > 1 else "")},
+            "roofline": {"kernel": "mmk gemm (tcgen05, persistent, fused epilogue)", "bound": "tensor",
+                         "achieved": round(g_tf, 1), "peak": sus, "unit": "TFLOP/s",
+                         "frac": round(g_tf / sus, 4) if sus else None, "peak_kind": f"{src} sustained bf16",
+                         "traffic": traffic.get("gemm"),
+                         "share_of_step": round(g["ms"] / ms_max, 4) if ms_max else None},
+            "roofline_step": {"achieved": round(enc_tf, 1), "peak": sus, "unit": "TFLOP/s",
+                              "frac": round(enc_tf / sus, 4),
+                              "note": "algorithmic encoder FLOPs of the whole step / step time"},
+            "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
+                            "achieved": round(v["work"] / (v["ms"] / 1e3) / (1e12 if k in ("gemm", "attention") else 1e9), 1)
+                            if v["ms"] else None,
+                            "unit": "TFLOP/s" if k in ("gemm", "attention") else "GB/s"}
+                        for k, v in kernels.items()},
+            "attention": {"achieved": round(a_tf, 1), "unit": "TFLOP/s", "frac": round(a_tf / sus, 4)},
+            "gpu_launches": launches,
+            "e2e": {"value": round(e_value, 3), "unit": "images/s", "h2d_bytes_per_step": h2d // args.steps,
+                    "d2h_bytes_per_step": d2h // args.steps,
+                    "path": "ImagePathExecutor.encode(stage_images(pinned host uint8)) + checksum D2H"},
+            "clocks": clk.result(),
+        }
+        if not args.no_cpu_baseline and world == 1:
+            threads = len(os.sched_getaffinity(0))
+            sample = dims[:args.cpu_sample_images]
+            dt = cpu_reference_time(spec, sample, ex.weights, threads)
+            line["cpu_baseline"] = {"value": round(len(sample) / dt, 4), "unit": "images/s", "cores": threads,
+                                    "kind": "port",
+                                    "sample": f"first {len(sample)} images of the workload "
+                                              f"({sum(tiles[:len(sample)])} tiles), oracle numpy preprocess + "
+                                              f"torch fp32 encoder, {dt:.1f} s"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

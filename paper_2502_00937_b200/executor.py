@@ -125,6 +125,7 @@ class ImagePathExecutor:
         seq = np.zeros(n + 1, np.int32)
         seq[1:] = np.cumsum(np.asarray(tiles, np.int64) * (P + 1))
         cu = torch.from_numpy(seq).pin_memory().to(self.device, non_blocking=True)
+        ops.set_attention_flops(cu, float(4 * np.sum(np.diff(seq).astype(np.float64) ** 2)))
         max_s = int(max(tiles)) * (P + 1)
         if enc.family == "mllama":
             tile_image, tile_slot = ops.tile_index(plan["tile_off"], n, total_tiles)

@@ -13,6 +13,52 @@ EPI_BF16, EPI_BF16_GELU, EPI_BF16_QUICKGELU, EPI_F32, EPI_RESID_F32 = range(5)
 ACT_EPI = {"gelu": EPI_BF16_GELU, "quick_gelu": EPI_BF16_QUICKGELU}
 
 
+class LaunchLog:
+    """Optional per-launch CUDA-event log (bench.py's live roofline).  When ``ops.LOG`` is set,
+    every wrapper records events around its single libmmk launch on the current stream."""
+
+    def __init__(self, timing: bool = True):
+        self.timing = timing
+        self.records = []  # (kind, work, start_event, end_event)
+        self.count = 0
+
+    def begin(self):
+        if not self.timing:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    def end(self, kind, work, start):
+        self.count += 1
+        if start is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.records.append((kind, work, start, e))
+
+    def summary(self):
+        """kind -> dict(launches, ms_total, work_total) (call after synchronize)."""
+        out = {}
+        for kind, work, s, e in self.records:
+            d = out.setdefault(kind, {"launches": 0, "ms": 0.0, "work": 0.0})
+            d["launches"] += 1
+            d["ms"] += s.elapsed_time(e)
+            d["work"] += work
+        return out
+
+
+LOG: LaunchLog | None = None
+
+
+def _begin():
+    return LOG.begin() if LOG is not None else None
+
+
+def _end(kind, work, start):
+    if LOG is not None:
+        LOG.end(kind, work, start)
+
+
 def _p(t):
     return None if t is None else t.data_ptr()
 
@@ -42,17 +88,21 @@ def tile_plan(w: torch.Tensor, h: torch.Tensor, spec, resize_mode: int | None = 
     bad = torch.empty(1, dtype=torch.int32, device=dev)
     if resize_mode is None:
         resize_mode = spec.encoder.resize_mode if spec.encoder is not None else 0
+    _t0 = _begin()
     _lib.check(_lib.lib.mmk_tile_plan(w.data_ptr(), h.data_ptr(), n, spec.tile_edge_px, spec.tokens_per_tile,
                                       spec.max_tiles_per_image, int(spec.thumbnail_tile), resize_mode,
                                       tiles.data_ptr(), tile_off.data_ptr(), tok_off.data_ptr(), geom.data_ptr(),
                                       ar_id.data_ptr(), bad.data_ptr(), _s()))
+    _end('tile_plan', 0, _t0)
     return {"tiles": tiles, "tile_off": tile_off, "tok_off": tok_off, "geom": geom, "ar_id": ar_id, "bad": bad}
 
 
 def tile_index(tile_off: torch.Tensor, n: int, total_tiles: int):
     tile_image = torch.empty(total_tiles, dtype=torch.int32, device=tile_off.device)
     tile_slot = torch.empty(total_tiles, dtype=torch.int32, device=tile_off.device)
+    _t0 = _begin()
     _lib.check(_lib.lib.mmk_tile_index(tile_off.data_ptr(), n, tile_image.data_ptr(), tile_slot.data_ptr(), _s()))
+    _end('tile_index', 0, _t0)
     return tile_image, tile_slot
 
 
@@ -63,10 +113,12 @@ def preprocess(src, src_off, w, h, tile_off, geom, n: int, total_tiles: int, spe
     P = (spec.tile_edge_px // enc.patch_px) ** 2
     if out is None:
         out = torch.empty(total_tiles * P, k_pad, dtype=torch.bfloat16, device=src.device)
+    _t0 = _begin()
     _lib.check(_lib.lib.mmk_preprocess(src.data_ptr(), src_off.data_ptr(), w.data_ptr(), h.data_ptr(),
                                        tile_off.data_ptr(), geom.data_ptr(), n, total_tiles, spec.tile_edge_px,
                                        enc.patch_px, k_pad, enc.resize_mode, int(spec.thumbnail_tile),
                                        scale3.data_ptr(), shift3.data_ptr(), out.data_ptr(), _s()))
+    _end('preprocess', float(src.numel()) + out.shape[0] * 3 * enc.patch_px ** 2 * 2.0, _t0)
     return out
 
 
@@ -82,9 +134,11 @@ def gemm(a: torch.Tensor, b: torch.Tensor, epilogue: int = EPI_BF16, bias=None, 
         if epilogue == EPI_RESID_F32:
             raise SpecError("gemm: RESID_F32 needs the residual tensor as `out`")
         out = torch.empty(m, n, dtype=torch.float32 if f32_out else torch.bfloat16, device=a.device)
+    _t0 = _begin()
     _lib.check(_lib.lib.mmk_gemm_bf16(a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), m, n, k, epilogue,
                                       _p(bias), out.data_ptr(), out.stride(0), float(gate), _p(aux),
                                       aux.stride(0) if aux is not None else 0, _s()))
+    _end('gemm', 2.0 * m * n * k, _t0)
     return out
 
 
@@ -93,10 +147,24 @@ def layernorm(x, gamma, beta, eps: float, out=None, out_f32: bool = False, tile_
     rows, d = x.shape
     if out is None:
         out = torch.empty(rows, d, dtype=torch.float32 if out_f32 else torch.bfloat16, device=x.device)
+    _t0 = _begin()
     _lib.check(_lib.lib.mmk_layernorm(x.data_ptr(), out.data_ptr(), int(out_f32), rows, d, gamma.data_ptr(),
                                       beta.data_ptr(), float(eps), _p(tile_add), _p(tile_image), _p(image_table),
                                       _p(tile_slot), rows_per_tile, slots, _s()))
+    _end('layernorm', x.numel() * 4.0 + out.numel() * out.element_size(), _t0)
     return out
+
+
+_SEQ_FLOPS: dict = {}
+
+
+def set_attention_flops(cu_seqlens, flops_per_head_dim: float):
+    """Register sum(4 * S_i^2) for a cu_seqlens tensor (host-known; avoids a device sync)."""
+    _SEQ_FLOPS[cu_seqlens.data_ptr()] = flops_per_head_dim
+
+
+def _attn_flops(cu_seqlens, heads, head_dim):
+    return _SEQ_FLOPS.get(cu_seqlens.data_ptr(), 0.0) * heads * head_dim
 
 
 def attention(qkv, cu_seqlens, n_seq: int, max_seqlen: int, heads: int, head_dim: int, out=None,
@@ -106,8 +174,10 @@ def attention(qkv, cu_seqlens, n_seq: int, max_seqlen: int, heads: int, head_dim
         out = torch.empty(T, heads * head_dim, dtype=torch.bfloat16, device=qkv.device)
     if scale is None:
         scale = head_dim ** -0.5
+    _t0 = _begin()
     _lib.check(_lib.lib.mmk_attention_varlen_bf16(qkv.data_ptr(), out.data_ptr(), cu_seqlens.data_ptr(), n_seq,
                                                   max_seqlen, heads, head_dim, float(scale), _s()))
+    _end('attention', _attn_flops(cu_seqlens, heads, head_dim), _t0)
     return out
 
 
@@ -118,11 +188,13 @@ def embed_tokens(patch_out, total_tiles: int, patches_per_tile: int, cls, pos, p
     rows = total_tiles * (patches_per_tile + 1)
     if out is None:
         out = torch.empty(rows, d, dtype=torch.float32, device=patch_out.device)
+    _t0 = _begin()
     _lib.check(_lib.lib.mmk_embed_tokens(patch_out.data_ptr(), _p(tile_image), _p(tile_slot), _p(image_ar),
                                          total_tiles, patches_per_tile, d, cls.data_ptr(), pos.data_ptr(),
                                          float(pos_scale), _p(tile_pos), float(tile_pos_scale), _p(pre_tile),
                                          float(pre_scale), slots, gamma.data_ptr(), beta.data_ptr(), float(eps),
                                          out.data_ptr(), _s()))
+    _end('embed', out.numel() * 8.0, _t0)
     return out
 
 
@@ -131,7 +203,9 @@ def pack_mllama(final_resid, inter, out=None):
     n_inter = inter.shape[0] if inter is not None else 0
     if out is None:
         out = torch.empty(rows, d * (1 + n_inter), dtype=torch.bfloat16, device=final_resid.device)
+    _t0 = _begin()
     _lib.check(_lib.lib.mmk_pack_mllama(final_resid.data_ptr(), _p(inter), n_inter, rows, d, out.data_ptr(), _s()))
+    _end('pack', out.numel() * 2.0 * 2, _t0)
     return out
 
 
@@ -139,13 +213,17 @@ def pack_drop_cls(src, tiles: int, tokens_per_tile: int, drop: int, out=None):
     d = src.shape[1]
     if out is None:
         out = torch.empty(tiles * (tokens_per_tile - drop), d, dtype=torch.bfloat16, device=src.device)
+    _t0 = _begin()
     _lib.check(_lib.lib.mmk_pack_drop_cls(src.data_ptr(), int(src.dtype == torch.float32), tiles, tokens_per_tile,
                                           drop, d, out.data_ptr(), _s()))
+    _end('pack', out.numel() * 4.0, _t0)
     return out
 
 
 def checksum(x, out=None):
     if out is None:
         out = torch.empty(1, dtype=torch.float32, device=x.device)
+    _t0 = _begin()
     _lib.check(_lib.lib.mmk_checksum_bf16(x.data_ptr(), x.numel(), out.data_ptr(), _s()))
+    _end('checksum', x.numel() * 2.0, _t0)
     return out
