@@ -8,6 +8,7 @@
 // This file holds the register-tiled flash-attention kernel (online softmax, exp2, bf16
 // mma.sync.m16n8k16 with fp32 accumulation, cp.async double-buffered K/V tiles).
 #include "sm100_common.cuh"
+#include <cstdlib>
 #include "mmk_internal.h"
 
 namespace mmk {
@@ -236,15 +237,27 @@ static int launch_attn_mma(const void* qkv, void* out, const int32_t* cu, int n_
 
 using namespace mmk;
 
+namespace mmk {
+template <int HD>
+int launch_attn_tc(const void* qkv, void* out, const int32_t* cu, int n_seq, int max_s, int heads, float scale,
+                   int64_t total_rows, cudaStream_t stream);
+}
+
 extern "C" int mmk_attention_varlen_bf16(const void* qkv, void* out, const int32_t* cu_seqlens, int32_t n_seq,
-                                         int32_t max_seqlen, int32_t heads, int32_t head_dim, float scale,
-                                         cudaStream_t stream) {
-  if (n_seq < 0 || heads <= 0 || max_seqlen < 0) return set_error(MMK_ERR_ARG, "attention: bad shape");
-  if (n_seq == 0 || max_seqlen == 0) return MMK_OK;
+                                         int32_t max_seqlen, int32_t total_tokens, int32_t heads, int32_t head_dim,
+                                         float scale, cudaStream_t stream) {
+  if (n_seq < 0 || heads <= 0 || max_seqlen < 0 || total_tokens < 0)
+    return set_error(MMK_ERR_ARG, "attention: bad shape");
+  if (head_dim != 64 && head_dim != 80)
+    return set_error(MMK_ERR_UNSUPPORTED, "attention: head_dim %d not in {64, 80}", head_dim);
+  if (n_seq == 0 || max_seqlen == 0 || total_tokens == 0) return MMK_OK;
   if (n_seq > 65535 || heads > 65535) return set_error(MMK_ERR_UNSUPPORTED, "attention: too many sequences/heads");
-  switch (head_dim) {
-    case 64: return launch_attn_mma<64>(qkv, out, cu_seqlens, n_seq, max_seqlen, heads, scale, stream);
-    case 80: return launch_attn_mma<80>(qkv, out, cu_seqlens, n_seq, max_seqlen, heads, scale, stream);
-    default: return set_error(MMK_ERR_UNSUPPORTED, "attention: head_dim %d not in {64, 80}", head_dim);
+  static const bool legacy = getenv("MMK_ATTN_LEGACY") != nullptr;  // A/B against the mma.sync baseline
+  if (legacy) {
+    if (head_dim == 64) return launch_attn_mma<64>(qkv, out, cu_seqlens, n_seq, max_seqlen, heads, scale, stream);
+    return launch_attn_mma<80>(qkv, out, cu_seqlens, n_seq, max_seqlen, heads, scale, stream);
   }
+  if (head_dim == 64)
+    return launch_attn_tc<64>(qkv, out, cu_seqlens, n_seq, max_seqlen, heads, scale, total_tokens, stream);
+  return launch_attn_tc<80>(qkv, out, cu_seqlens, n_seq, max_seqlen, heads, scale, total_tokens, stream);
 }

@@ -19,6 +19,18 @@ MMK_DEV uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 MMK_DEV uint32_t lane_id() { return threadIdx.x & 31; }
+// true on exactly one lane of a converged warp (elect.sync); keeps the surrounding code
+// warp-uniform so the compiler can hold descriptors / addresses in uniform registers
+MMK_DEV bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .b32 %%rx;\n\t.reg .pred %%px;\n\t"
+      "elect.sync %%rx|%%px, %1;\n\t"
+      "@%%px mov.s32 %0, 1;\n\t}"
+      : "+r"(pred)
+      : "r"(0xffffffffu));
+  return pred != 0;
+}
 MMK_DEV uint32_t warp_id_uniform() {
   return __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
 }
@@ -49,6 +61,18 @@ MMK_DEV bool mbar_try_wait(uint32_t bar_addr, uint32_t parity) {
       "selp.b32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
       : "r"(bar_addr), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// non-blocking probe: has the phase with this parity completed?
+MMK_DEV bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
   return ok != 0;
 }

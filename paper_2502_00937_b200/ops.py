@@ -176,7 +176,7 @@ def attention(qkv, cu_seqlens, n_seq: int, max_seqlen: int, heads: int, head_dim
         scale = head_dim ** -0.5
     _t0 = _begin()
     _lib.check(_lib.lib.mmk_attention_varlen_bf16(qkv.data_ptr(), out.data_ptr(), cu_seqlens.data_ptr(), n_seq,
-                                                  max_seqlen, heads, head_dim, float(scale), _s()))
+                                                  max_seqlen, T, heads, head_dim, float(scale), _s()))
     _end('attention', _attn_flops(cu_seqlens, heads, head_dim), _t0)
     return out
 
