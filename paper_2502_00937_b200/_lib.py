@@ -12,12 +12,9 @@ import os
 from pathlib import Path
 
 from .core import SpecError
+from .profiles import ProfileError
 
 LIB_PATH = Path(os.environ.get("MMK_LIB", Path(__file__).resolve().parent / "libmmk.so"))
-
-
-class ProfileError(ValueError):
-    """Unsupported configuration for a stage (same role as lmmsim.profiles.ProfileError)."""
 
 
 class MMKError(RuntimeError):

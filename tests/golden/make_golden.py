@@ -10,6 +10,7 @@ Outputs (tests/golden/):
                    ~8k generator-drawn dims (reference core.py:58-74)
   generator.json   reference workload.generate() request streams for several seeds/configs
                    (workload.py:222-296)
+  profile_llama.json  the reference's calibrated LatencyProfile for llama3.2-11b (export base)
   policies.json    split_by_tiles (policies.py:91-101), route_image (:104-124),
                    schedule_order (:153-173) and form_batch (engine.py:100-114) cases
 """
@@ -143,7 +144,16 @@ def policies():
                                                   separators=(",", ":")))
 
 
+def profile():
+    """The reference's own calibrated profile (profiles.py:400-470) — base for the export test."""
+    from lmmsim import profiles as rprof
+    spec = rcore.get_model_spec("llama3.2-11b")
+    prof = rprof.calibrate(rprof.load_calibration_targets(spec.name), spec)
+    (OUT / "profile_llama.json").write_text(json.dumps(prof.to_dict(), indent=1))
+
+
 if __name__ == "__main__":
+    profile()
     tiling()
     generator()
     policies()
