@@ -13,6 +13,7 @@
 //   warps 4..11 epilogue:     tcgen05.ld -> bias / activation / gated residual -> global
 // Epilogue of tile i overlaps the MMAs of tile i+1 via the two accumulator buffers.
 #include "sm100_common.cuh"
+#include <cstdlib>
 #include "mmk_internal.h"
 
 namespace mmk {
@@ -30,7 +31,22 @@ struct GemmSmem {
   static constexpr int kTotal = kBarOffset + 256 + 1024;  // + barriers + alignment slack
 };
 
-MMK_DEV float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
+// GELU(x) = x/2 (1 + erf(x / sqrt 2)), erf by Abramowitz-Stegun 7.1.26 (|error| < 1.5e-7, far
+// below the bf16 output rounding): one MUFU reciprocal, one MUFU exp2, 9 FMA-pipe ops.
+MMK_DEV float gelu_erf(float x) {
+  const float z = fabsf(x) * 0.70710678118654752f;
+  float t;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f, z, 1.0f)));
+  float p = fmaf(1.061405429f, t, -1.453152027f);
+  p = fmaf(p, t, 1.421413741f);
+  p = fmaf(p, t, -0.284496736f);
+  p = fmaf(p, t, 0.254829592f);
+  p *= t;
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-z * z * 1.4426950408889634f));
+  const float erf_abs = fmaf(-p, e, 1.0f);
+  return 0.5f * x * (1.0f + copysignf(erf_abs, x));
+}
 MMK_DEV float quick_gelu(float x) { return x / (1.0f + __expf(-1.702f * x)); }
 
 template <int EPI>
@@ -38,6 +54,55 @@ MMK_DEV float apply_act(float v) {
   if constexpr (EPI == MMK_EPI_BF16_GELU) return gelu_erf(v);
   else if constexpr (EPI == MMK_EPI_BF16_QUICKGELU) return quick_gelu(v);
   else return v;
+}
+
+// Fused epilogue for 32 consecutive accumulator columns of one output row (thread-owned row).
+template <int EPI>
+MMK_DEV void epilogue_chunk(const uint32_t (&r)[32], int row, int col, const float* __restrict__ bias, void* out,
+                            int64_t ldo, float gate, __nv_bfloat16* __restrict__ aux, int64_t ld_aux) {
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+  if (bias != nullptr) {
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + col + i));
+      v[i] += b4.x; v[i + 1] += b4.y; v[i + 2] += b4.z; v[i + 3] += b4.w;
+    }
+  }
+  if constexpr (EPI == MMK_EPI_F32) {
+    float* o = reinterpret_cast<float*>(out) + static_cast<int64_t>(row) * ldo + col;
+#pragma unroll
+    for (int i = 0; i < 32; i += 4)
+      *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+  } else if constexpr (EPI == MMK_EPI_RESID_F32) {
+    float* o = reinterpret_cast<float*>(out) + static_cast<int64_t>(row) * ldo + col;
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      float4 rr = *reinterpret_cast<const float4*>(o + i);
+      rr.x = fmaf(gate, v[i], rr.x);
+      rr.y = fmaf(gate, v[i + 1], rr.y);
+      rr.z = fmaf(gate, v[i + 2], rr.z);
+      rr.w = fmaf(gate, v[i + 3], rr.w);
+      v[i] = rr.x; v[i + 1] = rr.y; v[i + 2] = rr.z; v[i + 3] = rr.w;
+      *reinterpret_cast<float4*>(o + i) = rr;
+    }
+    if (aux != nullptr) {
+      __nv_bfloat16* ao = aux + static_cast<int64_t>(row) * ld_aux + col;
+#pragma unroll
+      for (int i = 0; i < 32; i += 8)
+        st_global_v4(ao + i, pack_bf16x2(v[i], v[i + 1]), pack_bf16x2(v[i + 2], v[i + 3]),
+                     pack_bf16x2(v[i + 4], v[i + 5]), pack_bf16x2(v[i + 6], v[i + 7]));
+    }
+  } else {
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + static_cast<int64_t>(row) * ldo + col;
+#pragma unroll
+    for (int i = 0; i < 32; i += 8)
+      st_global_v4(o + i, pack_bf16x2(apply_act<EPI>(v[i]), apply_act<EPI>(v[i + 1])),
+                   pack_bf16x2(apply_act<EPI>(v[i + 2]), apply_act<EPI>(v[i + 3])),
+                   pack_bf16x2(apply_act<EPI>(v[i + 4]), apply_act<EPI>(v[i + 5])),
+                   pack_bf16x2(apply_act<EPI>(v[i + 6]), apply_act<EPI>(v[i + 7])));
+  }
 }
 
 template <int BN, int STAGES, int EPI>
@@ -81,55 +146,59 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      const uint64_t pol_b = l2_policy_evict_last();  // weights: re-read by every M tile
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int m0 = (tile / n_tiles_n) * kGemmBM;
-        const int n0 = (tile % n_tiles_n) * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * S::kStageBytes;
-          uint8_t* sb = sa + S::kABytes;
+    // ------------------------------------------------------------ TMA producer (warp-uniform)
+    const uint64_t pol_b = l2_policy_evict_last();  // weights: re-read by every M tile
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const int m0 = (tile / n_tiles_n) * kGemmBM;
+      const int n0 = (tile % n_tiles_n) * BN;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t* sa = smem + stage * S::kStageBytes;
+        uint8_t* sb = sa + S::kABytes;
+        if (elect_one()) {
           mbar_arrive_expect_tx(&full_bar[stage], S::kStageBytes);
           tma_load_2d(&tmap_a, &full_bar[stage], sa, kb * kGemmBK, m0);
           tma_load_2d_hint(&tmap_b, &full_bar[stage], sb, kb * kGemmBK, n0, pol_b);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_bf16_f32(kGemmBM, BN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int t = 0;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
-        const int acc = t & 1;
-        const uint32_t acc_phase = (t >> 1) & 1;
-        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+    // ------------------------------------------------------------ MMA issuer (warp-uniform,
+    // one elected lane issues: descriptors stay in uniform registers)
+    constexpr uint32_t idesc = umma_idesc_bf16_f32(kGemmBM, BN);
+    const uint32_t smem_base = smem_u32(smem);
+    int stage = 0;
+    uint32_t phase = 0;
+    int t = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
+      const int acc = t & 1;
+      const uint32_t acc_phase = (t >> 1) & 1;
+      mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&full_bar[stage], phase);
-          tc_fence_after();
-          const uint32_t a_addr = smem_u32(smem + stage * S::kStageBytes);
-          const uint32_t b_addr = a_addr + S::kABytes;
-          const uint64_t adesc = umma_desc_sw128_kmajor(a_addr);
-          const uint64_t bdesc = umma_desc_sw128_kmajor(b_addr);
+        const uint32_t a_addr = smem_base + stage * S::kStageBytes;
+        const uint64_t adesc = umma_desc_sw128_kmajor(a_addr);
+        const uint64_t bdesc = umma_desc_sw128_kmajor(a_addr + S::kABytes);
+        if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < kGemmBK / 16; ++k) {
             // +32 bytes per K=16 step inside the 128-byte swizzle row (desc unit = 16 B)
             umma_bf16_ss(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
           }
           umma_commit(&empty_bar[stage]);  // frees the smem slot when these MMAs retire
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&tfull_bar[acc]);  // accumulator ready for the epilogue
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+      if (elect_one()) umma_commit(&tfull_bar[acc]);  // accumulator ready for the epilogue
+      __syncwarp();
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
@@ -154,49 +223,7 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
         tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + acc * BN + col_in_tile, r);
         tmem_ld_wait();
         if (!row_ok || col >= N) continue;
-        float v[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        if (bias != nullptr) {
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + col + i));
-            v[i] += b4.x; v[i + 1] += b4.y; v[i + 2] += b4.z; v[i + 3] += b4.w;
-          }
-        }
-        if constexpr (EPI == MMK_EPI_F32) {
-          float* o = reinterpret_cast<float*>(out) + static_cast<int64_t>(row) * ldo + col;
-#pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-        } else if constexpr (EPI == MMK_EPI_RESID_F32) {
-          float* o = reinterpret_cast<float*>(out) + static_cast<int64_t>(row) * ldo + col;
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            float4 rr = *reinterpret_cast<const float4*>(o + i);
-            rr.x = fmaf(gate, v[i], rr.x);
-            rr.y = fmaf(gate, v[i + 1], rr.y);
-            rr.z = fmaf(gate, v[i + 2], rr.z);
-            rr.w = fmaf(gate, v[i + 3], rr.w);
-            v[i] = rr.x; v[i + 1] = rr.y; v[i + 2] = rr.z; v[i + 3] = rr.w;
-            *reinterpret_cast<float4*>(o + i) = rr;
-          }
-          if (aux != nullptr) {
-            __nv_bfloat16* ao = aux + static_cast<int64_t>(row) * ld_aux + col;
-#pragma unroll
-            for (int i = 0; i < 32; i += 8)
-              st_global_v4(ao + i, pack_bf16x2(v[i], v[i + 1]), pack_bf16x2(v[i + 2], v[i + 3]),
-                           pack_bf16x2(v[i + 4], v[i + 5]), pack_bf16x2(v[i + 6], v[i + 7]));
-          }
-        } else {
-          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + static_cast<int64_t>(row) * ldo + col;
-#pragma unroll
-          for (int i = 0; i < 32; i += 8)
-            st_global_v4(o + i, pack_bf16x2(apply_act<EPI>(v[i]), apply_act<EPI>(v[i + 1])),
-                         pack_bf16x2(apply_act<EPI>(v[i + 2]), apply_act<EPI>(v[i + 3])),
-                         pack_bf16x2(apply_act<EPI>(v[i + 4]), apply_act<EPI>(v[i + 5])),
-                         pack_bf16x2(apply_act<EPI>(v[i + 6]), apply_act<EPI>(v[i + 7])));
-        }
+        epilogue_chunk<EPI>(r, row, col, bias, out, ldo, gate, aux, ld_aux);
       }
       tc_fence_before();
       __syncwarp();
@@ -208,6 +235,227 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc<2 * BN>(tmem_base);
+}
+
+// ------------------------------------------------------------------ CTA-pair variant
+// cta_group::2: a cluster of 2 CTAs (one per SM of a TPC) computes a 256 x BN2 tile with
+// tcgen05.mma M=256.  Each CTA stages its own 128 rows of A and its own BN2/2 rows of B per
+// k-block (half the shared-memory traffic of the single-CTA kernel per SM); the leader CTA issues
+// the MMAs, which read both CTAs' smem and write both CTAs' TMEM (128 lanes x BN2 cols each).
+// Barriers: `full` lives in the leader (TMA completions of both CTAs counted there), `empty` and
+// `tfull` are multicast by the leader's tcgen05.commit to both CTAs, `tempty` lives in the leader
+// and counts the epilogue warps of both CTAs.
+constexpr int kGemm2BN = 256;
+template <int STAGES>
+struct Gemm2Smem {
+  static constexpr int kABytes = 128 * kGemmBK * 2;             // this CTA's 128 rows of A
+  static constexpr int kBBytes = (kGemm2BN / 2) * kGemmBK * 2;  // this CTA's half of B
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kEpiOffset = STAGES * kStageBytes;       // 8 warps x 2 x [32 rows][128 B]
+  static constexpr int kEpiBytes = 8 * 2 * 4096;
+  static constexpr int kBarOffset = kEpiOffset + kEpiBytes;
+  static constexpr int kTotal = kBarOffset + 256 + 1024;
+};
+
+// bf16 epilogue through shared memory + TMA store: 32 rows x 64 cols per warp per step, staged in
+// a 128B-swizzled [32][128 B] buffer (conflict-free 16-byte st.shared), written by one bulk
+// tensor store; two buffers per warp so the store of one chunk overlaps the next chunk.
+template <int EPI>
+MMK_DEV void epilogue_bf16_tma(const uint32_t (&r0)[32], const uint32_t (&r1)[32], int col, int row0, uint32_t lane,
+                               const float* __restrict__ bias, uint8_t* buf, const CUtensorMap* tmap_out) {
+  uint32_t w[32];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t (&r)[32] = h ? r1 : r0;
+#pragma unroll
+    for (int i = 0; i < 32; i += 2) {
+      float a = __uint_as_float(r[i]), b = __uint_as_float(r[i + 1]);
+      if (bias != nullptr) {
+        a += __ldg(bias + col + 32 * h + i);
+        b += __ldg(bias + col + 32 * h + i + 1);
+      }
+      w[16 * h + i / 2] = pack_bf16x2(apply_act<EPI>(a), apply_act<EPI>(b));
+    }
+  }
+  if (lane == 0) tma_store_wait_read<1>();  // this buffer's previous store has been read out
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {  // 16-byte chunk j = columns 8j..8j+7 of this row
+    const uint32_t dst = smem_u32(buf + lane * 128 + ((j ^ (lane & 7)) << 4));
+    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(dst), "r"(w[4 * j]), "r"(w[4 * j + 1]),
+                 "r"(w[4 * j + 2]), "r"(w[4 * j + 3])
+                 : "memory");
+  }
+  fence_proxy_async();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(tmap_out, buf, col, row0);
+    tma_store_commit();
+  }
+}
+
+template <int STAGES, int EPI>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                      const __grid_constant__ CUtensorMap tmap_out, int M, int N, int K, const float* __restrict__ bias, void* __restrict__ out, int64_t ldo,
+                      float gate, __nv_bfloat16* __restrict__ aux, int64_t ld_aux) {
+  using S = Gemm2Smem<STAGES>;
+  constexpr int BN = kGemm2BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S::kBarOffset);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;  // [2]
+  uint64_t* tempty_bar = tfull_bar + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const uint32_t warp = warp_id_uniform();
+  const uint32_t lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int n_tiles_n = N / BN;
+  const int n_tiles = ((M + 255) / 256) * n_tiles_n;
+  const int num_kb = (K + kGemmBK - 1) / kGemmBK;
+  const int first = static_cast<int>(cluster_id_x()), step = static_cast<int>(n_clusters_x());
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 16);  // 8 epilogue warps x 2 CTAs
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_2sm<2 * BN>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer (both CTAs)
+    const uint64_t pol_a = l2_policy_evict_first();
+    const uint64_t pol_b = l2_policy_evict_last();
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = first; tile < n_tiles; tile += step) {
+      const int m0 = (tile / n_tiles_n) * 256 + rank * 128;
+      const int n0 = (tile % n_tiles_n) * BN + rank * (BN / 2);
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t* sa = smem + stage * S::kStageBytes;
+        uint8_t* sb = sa + S::kABytes;
+        const uint32_t fb = mapa_shared(smem_u32(&full_bar[stage]), 0);  // leader's barrier
+        if (elect_one()) {
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
+          tma_load_2d_2sm(&tmap_a, fb, sa, kb * kGemmBK, m0, pol_a);
+          tma_load_2d_2sm(&tmap_b, fb, sb, kb * kGemmBK, n0, pol_b);
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer (leader CTA only)
+    if (leader) {
+      constexpr uint32_t idesc = umma_idesc_bf16_f32(256, BN);
+      const uint32_t smem_base = smem_u32(smem);
+      int stage = 0;
+      uint32_t phase = 0;
+      int t = 0;
+      for (int tile = first; tile < n_tiles; tile += step, ++t) {
+        const int acc = t & 1;
+        const uint32_t acc_phase = (t >> 1) & 1;
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_base + stage * S::kStageBytes;
+          const uint64_t adesc = umma_desc_sw128_kmajor(a_addr);
+          const uint64_t bdesc = umma_desc_sw128_kmajor(a_addr + S::kABytes);
+          if (elect_one()) {
+#pragma unroll
+            for (int k = 0; k < kGemmBK / 16; ++k)
+              umma_bf16_ss_2sm(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            umma_commit_2sm(&empty_bar[stage], 0x3);
+          }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (elect_one()) umma_commit_2sm(&tfull_bar[acc], 0x3);
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------ epilogue (both CTAs, own 128 rows)
+    constexpr bool kTmaStore = EPI == MMK_EPI_BF16 || EPI == MMK_EPI_BF16_GELU || EPI == MMK_EPI_BF16_QUICKGELU;
+    const uint32_t q = warp & 3;
+    const uint32_t half = (warp - 4) >> 2;
+    constexpr int kColsPerWarp = BN / 2;
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
+    uint8_t* ebuf = smem + S::kEpiOffset + (warp - 4) * 2 * 4096;
+    int sb = 0;
+    int t = 0;
+    for (int tile = first; tile < n_tiles; tile += step, ++t) {
+      const int acc = t & 1;
+      const uint32_t acc_phase = (t >> 1) & 1;
+      const int m0 = (tile / n_tiles_n) * 256 + rank * 128;
+      const int n0 = (tile % n_tiles_n) * BN;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tm_row = tmem_base + ((q * 32u) << 16) + acc * BN;
+      if constexpr (kTmaStore) {
+#pragma unroll 1
+        for (int c = 0; c < kColsPerWarp / 64; ++c) {
+          const int col_in_tile = half * kColsPerWarp + c * 64;
+          uint32_t r0[32], r1[32];
+          tmem_ld_32x32b_x32(tm_row + col_in_tile, r0);
+          tmem_ld_32x32b_x32(tm_row + col_in_tile + 32, r1);
+          tmem_ld_wait();
+          if (c == kColsPerWarp / 64 - 1) {  // accumulator fully read: release it early
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
+          }
+          epilogue_bf16_tma<EPI>(r0, r1, n0 + col_in_tile, m0 + static_cast<int>(q) * 32, lane, bias,
+                                 ebuf + sb * 4096, &tmap_out);
+          sb ^= 1;
+        }
+      } else {
+        const int row = m0 + q * 32 + lane;
+        const bool row_ok = row < M;
+#pragma unroll 1
+        for (int c = 0; c < kColsPerWarp / 32; ++c) {
+          const int col_in_tile = half * kColsPerWarp + c * 32;
+          const int col = n0 + col_in_tile;
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tm_row + col_in_tile, r);
+          tmem_ld_wait();
+          if (!row_ok) continue;
+          epilogue_chunk<EPI>(r, row, col, bias, out, ldo, gate, aux, ld_aux);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
+      }
+    }
+    if constexpr (kTmaStore) {
+      if (lane == 0) tma_store_wait<0>();
+      __syncwarp();
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_2sm<2 * BN>(tmem_base);
 }
 
 // ------------------------------------------------------------------ host side
@@ -245,6 +493,53 @@ static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, i
   }
 }
 
+
+template <int STAGES, int EPI>
+static int launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, int M, int N, int K,
+                           const float* bias,
+                           void* out, int64_t ldo, float gate, __nv_bfloat16* aux, int64_t ld_aux,
+                           cudaStream_t stream) {
+  using S = Gemm2Smem<STAGES>;
+  auto kern = gemm_bf16_tcgen05_2sm<STAGES, EPI>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
+    if (e != cudaSuccess) return set_cuda_error(e, "gemm2: cudaFuncSetAttribute");
+    attr_done = true;
+  }
+  const int tiles = ((M + 255) / 256) * (N / kGemm2BN);
+  const int pairs_max = num_sms() / 2;
+  const int pairs = tiles < pairs_max ? tiles : pairs_max;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = S::kTotal;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux);
+  if (e != cudaSuccess) return set_cuda_error(e, "gemm2: launch");
+  return MMK_OK;
+}
+
+template <int STAGES>
+static int dispatch_epi_2sm(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, int M,
+                            int N, int K, const float* bias, void* out, int64_t ldo, float gate,
+                            __nv_bfloat16* aux, int64_t ld_aux, cudaStream_t s) {
+  switch (epi) {
+    case MMK_EPI_BF16: return launch_gemm_2sm<STAGES, MMK_EPI_BF16>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
+    case MMK_EPI_BF16_GELU: return launch_gemm_2sm<STAGES, MMK_EPI_BF16_GELU>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
+    case MMK_EPI_BF16_QUICKGELU: return launch_gemm_2sm<STAGES, MMK_EPI_BF16_QUICKGELU>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
+    case MMK_EPI_F32: return launch_gemm_2sm<STAGES, MMK_EPI_F32>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
+    case MMK_EPI_RESID_F32: return launch_gemm_2sm<STAGES, MMK_EPI_RESID_F32>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
+    default: return set_error(MMK_ERR_ARG, "gemm: unknown epilogue %d", epi);
+  }
+}
 }  // namespace mmk
 
 using namespace mmk;
@@ -263,7 +558,24 @@ extern "C" int mmk_gemm_bf16(const void* a, int64_t lda, const void* b, int64_t 
   if (ldo % (f32_out ? 4 : 8) != 0) return set_error(MMK_ERR_ARG, "gemm: ldo misaligned");
   if (aux != nullptr && (epilogue != MMK_EPI_RESID_F32 || ld_aux % 8 != 0))
     return set_error(MMK_ERR_ARG, "gemm: aux output only with RESID_F32 and 16B-aligned rows");
-  // BN choice: 256 unless that leaves most SMs idle.
+  // Kernel choice: CTA pairs (M=256 x N=256 tiles) when N splits into 256-wide tiles and there
+  // are enough tiles to occupy the pairs; otherwise the single-CTA kernel with BN 256 or 128.
+  static const bool no_2sm = getenv("MMK_GEMM_NO_2SM") != nullptr;  // A/B switch for profiling
+  const int tiles2 = ((m + 255) / 256) * (n / 256);
+  if (!no_2sm && n % 256 == 0 && tiles2 >= num_sms() / 2) {
+    CUtensorMap ta, tb;
+    int rc = make_tmap_2d_bf16(&ta, a, k, m, lda, kGemmBK, 128, true);
+    if (rc) return rc;
+    rc = make_tmap_2d_bf16(&tb, b, k, n, ldb, kGemmBK, 128, true);
+    if (rc) return rc;
+    CUtensorMap to = tb;  // output map: bf16 epilogues only ([32 rows][64 cols], 128B swizzle)
+    if (!f32_out) {
+      rc = make_tmap_2d_bf16(&to, out, n, m, ldo, 64, 32, true);
+      if (rc) return rc;
+    }
+    return dispatch_epi_2sm<5>(epilogue, ta, tb, to, m, n, k, bias, out, ldo, gate,
+                               reinterpret_cast<__nv_bfloat16*>(aux), ld_aux, stream);
+  }
   const int tiles256 = ((m + kGemmBM - 1) / kGemmBM) * ((n + 255) / 256);
   const bool use128 = (n % 256 != 0) || tiles256 < num_sms();
   CUtensorMap ta, tb;
