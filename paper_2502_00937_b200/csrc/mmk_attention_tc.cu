@@ -31,6 +31,10 @@ __device__ long long g_attn_trace[3][64][8];
 #define TR(role, j, ev)
 #endif
 
+#ifndef MMK_POLY8
+#define MMK_POLY8 3  // pairs out of every 8 whose exp2 runs as an FMA-pipe polynomial
+#endif
+
 constexpr int kTcBQ = 128;
 constexpr int kTcBKV = 128;
 constexpr int kTcThreads = 320;
@@ -82,8 +86,9 @@ MMK_DEV float2 exp2_poly2(float2 x) {
   q = __ffma2_rn(q, f, make_float2(0.6931210339915522f, 0.6931210339915522f));
   q = __ffma2_rn(q, f, make_float2(0.9999244814555215f, 0.9999244814555215f));
   float2 e;
-  e.x = __uint_as_float(__float_as_uint(q.x) + (__float_as_uint(t.x) << 23));
-  e.y = __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(t.y) << 23));
+  // exponent added in the integer domain (LEA on the ALU pipe, not IMAD on the FMA pipe)
+  e.x = __uint_as_float(__float_as_uint(q.x) + __funnelshift_l(0u, __float_as_uint(t.x), 23));
+  e.y = __uint_as_float(__float_as_uint(q.y) + __funnelshift_l(0u, __float_as_uint(t.y), 23));
   return e;
 }
 
@@ -309,7 +314,7 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_main, const __grid_constant__
         for (int i = 0; i < 64; ++i) {
           const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), sc2, nm2);
           float2 e;
-          if ((i & 7) < 4) {
+          if ((i & 7) < MMK_POLY8) {
             e = exp2_poly2(x);
           } else {
             e.x = fast_exp2(x.x);

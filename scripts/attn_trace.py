@@ -2,7 +2,7 @@
 import ctypes, os, sys
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-os.environ["MMK_LIB"] = os.path.join(ROOT, "debug", "libmmk_trace.so")
+os.environ["MMK_LIB"] = os.environ.get("MMK_TRACE_LIB", os.path.join(ROOT, "debug", "libmmk_trace.so"))
 sys.path.insert(0, ROOT)
 import torch
 from paper_2502_00937_b200 import _lib, ops
@@ -27,3 +27,11 @@ for j in range(12):
 for j in (20, 30, 40):
     d0 = np.diff(buf[0, j, :6]); d1 = np.diff(buf[1, j, :6])
     print(f"j={j} WG0 deltas {d0.tolist()} WG1 deltas {d1.tolist()} period {buf[0, j+1, 1]-buf[0, j, 1]}")
+s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+s.record()
+for _ in range(10):
+    ops.attention(qkv, cu, len(lens), max(lens), heads, hd)
+e.record()
+torch.cuda.synchronize()
+ms = s.elapsed_time(e) / 10
+print(f"time {ms:.3f} ms  {sum(4.0 * L * L * heads * hd for L in lens) / ms / 1e9:.0f} TF/s (trace build)")
