@@ -96,6 +96,17 @@ def stage_images(images, device="cuda", pinned: bool = True, stream=None) -> Ima
                       h2d_bytes=total + meta.nbytes)
 
 
+@dataclass
+class CapturedEncode:
+    graph: "torch.cuda.CUDAGraph"
+    batch: ImageBatch
+    output: PackedBatch
+
+    def replay(self) -> PackedBatch:
+        self.graph.replay()
+        return self.output
+
+
 class ImagePathExecutor:
     """preprocess -> encode -> pack for one model on one GPU (one process per GPU)."""
 
@@ -122,10 +133,9 @@ class ImagePathExecutor:
                                  total_tiles, spec, self.encoder.k_pad, self.encoder.norm_scale,
                                  self.encoder.norm_shift)
         # attention sequences: all tokens of one image (images never attend to each other)
-        seq = np.zeros(n + 1, np.int32)
-        seq[1:] = np.cumsum(np.asarray(tiles, np.int64) * (P + 1))
-        cu = torch.from_numpy(seq).pin_memory().to(self.device, non_blocking=True)
-        ops.set_attention_flops(cu, float(4 * np.sum(np.diff(seq).astype(np.float64) ** 2)))
+        seq_len = np.asarray(tiles, np.float64) * (P + 1)
+        cu = (plan["tile_off"] * (P + 1)).to(torch.int32)  # device-side: capturable in a CUDA graph
+        ops.set_attention_flops(cu, float(4 * np.sum(seq_len ** 2)))
         max_s = int(max(tiles)) * (P + 1)
         if enc.family == "mllama":
             tile_image, tile_slot = ops.tile_index(plan["tile_off"], n, total_tiles)
@@ -134,6 +144,16 @@ class ImagePathExecutor:
             emb = self.encoder.forward(patches, total_tiles, cu, n, max_s)
         return PackedBatch(embeds=emb, tok_offsets=plan["tok_off"], tiles=tiles,
                            image_tokens=[t * spec.tokens_per_tile for t in tiles])
+
+    def capture(self, batch: ImageBatch) -> "CapturedEncode":
+        """Record ``encode(batch)`` as a CUDA graph (static shapes: same images each replay, or
+        new pixels copied into ``batch.src``).  Replay launches the whole path with one call."""
+        self.encode(batch)  # first run outside capture: kernel attributes, allocator warm-up
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            out = self.encode(batch)
+        return CapturedEncode(graph=g, batch=batch, output=out)
 
     def encode_images(self, images, pinned: bool = True) -> PackedBatch:
         return self.encode(stage_images(images, self.device, pinned))
