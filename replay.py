@@ -1,0 +1,86 @@
+#!/usr/bin/env python
+"""BASELINE configs[4]: bursty heavy-tailed multimodal trace (1-8 images/request) replayed in real
+time through the modality-aware batcher on 1..N B200 (one image instance per GPU, rank 0 is
+also the LLM-backend rank that joins the shards).
+
+    python replay.py [--duration-s 20] [--rate 10] [--burst-mult 3] [--max-batch 8]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 replay.py ...
+
+Prints one JSON line (rank 0): image-path latency percentiles (nearest-rank, reference
+metrics.py:12-18), achieved images/s, batches, plus the trace description.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+IMAGES_PER_REQUEST = {1: 0.30, 2: 0.20, 3: 0.15, 4: 0.10, 5: 0.10, 6: 0.05, 7: 0.05, 8: 0.05}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="llama3.2-11b")
+    ap.add_argument("--duration-s", type=float, default=20.0)
+    ap.add_argument("--rate", type=float, default=8.0, help="requests/s per GPU outside bursts")
+    ap.add_argument("--burst-mult", type=float, default=3.0)
+    ap.add_argument("--max-batch", type=int, default=8)
+    ap.add_argument("--scheduler", default="slo_priority", choices=["fifo", "slo_priority"])
+    ap.add_argument("--ms-per-tile", type=float, default=5.0, help="routing cost model (measured ~4.9 on B200)")
+    ap.add_argument("--seed", type=int, default=0)
+    args = ap.parse_args()
+
+    import torch
+    import torch.distributed as dist
+    from paper_2502_00937_b200 import core, policies, workload
+    from paper_2502_00937_b200.executor import ImagePathExecutor
+    from paper_2502_00937_b200.service import ImagePathService, ShardChannel
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    ctrl = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        ctrl = dist.new_group(backend="gloo")
+    spec = core.get_model_spec(args.model)
+    horizon = args.duration_s * 1000.0
+    burst = workload.BurstEpisode(start_ms=0.4 * horizon, duration_ms=0.2 * horizon, rate_multiplier=args.burst_mult)
+    cfg = workload.GeneratorConfig(model=spec, base_rate=args.rate * world, image_request_fraction=1.0,
+                                   images_per_request=dict(IMAGES_PER_REQUEST), burst_episodes=(burst,),
+                                   seed=args.seed)
+    reqs = workload.generate(cfg, horizon)
+    ex = ImagePathExecutor(spec, seed=0)
+    # warm the executor (kernel attributes, allocator) outside the replay clock
+    import numpy as np
+    ex.encode_images([np.zeros((560, 560, 3), np.uint8)] * 2)
+    torch.cuda.synchronize()
+    pol = policies.PolicySet(router=policies.RouterKind.LEAST_PENDING,
+                             scheduler=policies.SchedulerKind(args.scheduler), max_fanout=8, aging_slo_fraction=0.5)
+    svc = ImagePathService(spec, ex, rank=rank, world=world, policies=pol, max_batch={"encode": args.max_batch},
+                           cost_ms=lambda tiles: args.ms_per_tile * tiles, ttft_slo_ms=2000.0)
+    chan = ShardChannel(rank, world, torch.device("cuda", local), torch.bfloat16, ctrl_group=ctrl) if world > 1 else None
+    res = svc.replay(reqs, channel=chan, barrier=(dist.barrier if world > 1 else None))
+    if rank == 0:
+        s = res.summary()
+        n_img = sum(len(r.images) for r in reqs)
+        line = {"metric": "image-path latency under a bursty trace", "n_gpus": world, **s,
+                "trace": {"generator": "reference workload.generate", "seed": args.seed, "duration_s": args.duration_s,
+                          "rate_req_s": args.rate * world, "burst": [burst.start_ms, burst.duration_ms, burst.rate_multiplier],
+                          "images_per_request": IMAGES_PER_REQUEST, "requests": len(reqs), "images": n_img},
+                "batcher": {"router": "least_pending", "scheduler": args.scheduler, "max_batch_encode": args.max_batch},
+                "model": spec.name}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
