@@ -1,16 +1,15 @@
 // mmk_attention_tc.cu — K5 on 5th-generation tensor cores: varlen non-causal flash attention
 // with S = Q K^T and O = P V accumulated in TMEM (tcgen05.mma), Q/K/V tiles staged by TMA.
 //
-// CTA = two 128-row query tiles of one (sequence, head); warp roles:
-//   warps 0-3  softmax WG0 (query tile 0, TMEM lanes 0-127 = rows)
-//   warps 4-7  softmax WG1 (query tile 1)
-//   warp 8     TMA producer (Q once; K/V 128-key tiles into a STAGES-deep ring)
-//   warp 9     MMA issuer (single thread) + TMEM allocator
-// TMEM (512 columns): S0 [0,128) S1 [128,256) O0 [256,256+hd) O1 [384,384+hd).  A softmax
+// CTA = NQ 128-row query tiles of one (sequence, head), KV tiles of BKV keys; warp roles:
+//   warps 4t..4t+3   softmax warpgroup t (query tile t, TMEM lanes 0-127 = rows)
+//   warp 4*NQ        TMA producer (Q once; K/V tiles into a STAGES-deep ring)
+//   warp 4*NQ + 1    MMA issuer (warp-uniform, one elected lane) + TMEM allocator
+// TMEM (512 columns): S_t at [t*BKV, (t+1)*BKV), O_t after them (hd columns each).  A softmax
 // warpgroup releases its S buffer as soon as the scores are in registers (s_free), so the MMA
-// thread issues S_t(j+1) = Q_t K(j+1)^T while the exponentials of tile j are still being
+// warp issues S_t(j+1) = Q_t K(j+1)^T while the exponentials of tile j are still being
 // computed; P (bf16) goes to a 128B-swizzled shared-memory tile (K-major A operand of the PV
-// MMA).  Per KV tile j the MMA thread issues S0(j), S1(j), then PV0(j-1), PV1(j-1).
+// MMA).  Per KV tile j the MMA warp issues S_0..S_{NQ-1}(j), then PV_0..PV_{NQ-1}(j-1).
 // Online softmax in base 2 with a lazily updated running max (rescale O only when the row max
 // grows by more than 2^8), so O is rarely touched.
 //
@@ -18,6 +17,7 @@
 // 32B-swizzled block (1 k-step); V is the MN-major B operand, split into N=64 (128B swizzle)
 // and N=16 (32B swizzle) MMAs.  head_dim 64 uses the first block only.
 #include "sm100_common.cuh"
+#include <cstdlib>
 #include "mmk_internal.h"
 
 namespace mmk {
@@ -36,25 +36,29 @@ __device__ long long g_attn_trace[3][64][8];
 #endif
 
 constexpr int kTcBQ = 128;
-constexpr int kTcBKV = 128;
-constexpr int kTcThreads = 320;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
-template <int HD>
+template <int HD, int BKV, int NQ>
 struct TcAttnCfg {
-  static constexpr bool kRem = (HD % 64) != 0;           // has a 16-wide remainder block
-  static constexpr int kMain = 64;                        // main block width (elements)
-  static constexpr int kMainBytes = 128 * 64 * 2;         // one 128-row x 64-col tile
-  static constexpr int kRemBytes = kRem ? 128 * 16 * 2 : 0;
-  static constexpr int kTileBytes = kMainBytes + kRemBytes;  // Q, K or V tile
-  static constexpr int STAGES = 3;
-  static constexpr int kQOff = 0;                         // Q0, Q1
-  static constexpr int kKVOff = 2 * kTileBytes;           // stage s: K then V
-  static constexpr int kStageBytes = 2 * kTileBytes;
-  static constexpr int kPOff = kKVOff + STAGES * kStageBytes;   // P0, P1: [2 blocks][128 rows][128 B]
-  static constexpr int kPBytes = 128 * 128 * 2;
-  static constexpr int kBarOff = kPOff + 2 * kPBytes;
+  static constexpr bool kRem = (HD % 64) != 0;               // has a 16-wide remainder block
+  static constexpr int kQMain = kTcBQ * 64 * 2;              // Q tile: 128 rows x 64 cols
+  static constexpr int kQBytes = kQMain + (kRem ? kTcBQ * 16 * 2 : 0);
+  static constexpr int kKVMain = BKV * 64 * 2;               // K or V tile: BKV rows x 64 cols
+  static constexpr int kKVBytes = kKVMain + (kRem ? BKV * 16 * 2 : 0);
+  static constexpr int STAGES = BKV == 128 ? 3 : 4;
+  static constexpr int kQOff = 0;
+  static constexpr int kKVOff = NQ * kQBytes;
+  static constexpr int kStageBytes = 2 * kKVBytes;           // K then V
+  static constexpr int kPOff = kKVOff + STAGES * kStageBytes;  // P_t: [BKV/64 blocks][128 rows][128 B]
+  static constexpr int kPBlock = kTcBQ * 128;
+  static constexpr int kPBytes = (BKV / 64) * kPBlock;
+  static constexpr int kBarOff = kPOff + NQ * kPBytes;
   static constexpr int kSmem = kBarOff + 256 + 1024;
+  static constexpr int kThreads = 32 * (4 * NQ + 2);
+  static constexpr int kOBase = NQ * BKV;                    // TMEM column of O_0
+  static constexpr int kOStride = (512 - NQ * BKV) / NQ >= 128 ? 128 : 96;
+  static_assert(kOBase + (NQ - 1) * kOStride + HD <= 512, "TMEM overflow");
+  static_assert(kSmem <= 232448, "shared memory overflow");
 };
 
 MMK_DEV float fast_exp2(float x) {
@@ -92,11 +96,13 @@ MMK_DEV float2 exp2_poly2(float2 x) {
   return e;
 }
 
-template <int HD>
-__global__ void __maxnreg__(168)
-attn_fwd_tc(const __grid_constant__ CUtensorMap tm_main, const __grid_constant__ CUtensorMap tm_rem,
+template <int HD, int BKV, int NQ>
+__global__ void __maxnreg__(NQ == 2 ? 168 : 128)
+attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_q_rem,
+            const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_kv_rem,
             __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ cu_seqlens, int heads, float scale_log2) {
-  using C = TcAttnCfg<HD>;
+  using C = TcAttnCfg<HD, BKV, NQ>;
+  constexpr int kTmaWarp = 4 * NQ, kMmaWarp = 4 * NQ + 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
@@ -104,35 +110,39 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_main, const __grid_constant__
   uint64_t* k_full = bars + 1;                 // [STAGES]
   uint64_t* v_full = k_full + C::STAGES;       // [STAGES]
   uint64_t* kv_empty = v_full + C::STAGES;     // [STAGES]
-  uint64_t* s_full = kv_empty + C::STAGES;     // [2] MMA -> softmax: S_t ready
-  uint64_t* s_free = s_full + 2;               // [2] softmax -> MMA: S_t consumed
-  uint64_t* p_full = s_free + 2;               // [2] softmax -> MMA: P_t in smem (+ O_t rescaled)
-  uint64_t* pv_done = p_full + 2;              // [2] MMA -> softmax: PV_t retired
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
+  uint64_t* s_full = kv_empty + C::STAGES;     // [NQ] MMA -> softmax: S_t ready
+  uint64_t* s_free = s_full + NQ;              // [NQ] softmax -> MMA: S_t consumed
+  uint64_t* p_full = s_free + NQ;              // [NQ] softmax -> MMA: P_t in smem (+ O_t rescaled)
+  uint64_t* pv_done = p_full + NQ;             // [NQ] MMA -> softmax: PV_t retired
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + NQ);
 
   const int seq = blockIdx.y, head = blockIdx.z;
   const int s_begin = cu_seqlens[seq];
   const int len = cu_seqlens[seq + 1] - s_begin;
-  const int q0 = blockIdx.x * 2 * kTcBQ;
+  const int q0 = blockIdx.x * NQ * kTcBQ;
   if (q0 >= len) return;
-  const int n_qt = (q0 + kTcBQ < len) ? 2 : 1;
-  const int nkv = (len + kTcBKV - 1) / kTcBKV;
+  const int n_qt = min(NQ, (len - q0 + kTcBQ - 1) / kTcBQ);
+  const int nkv = (len + BKV - 1) / BKV;
   const int d_model = heads * HD;
   const int col_q = head * HD, col_k = d_model + head * HD, col_v = 2 * d_model + head * HD;
 
   const uint32_t warp = warp_id_uniform();
   const uint32_t lane = lane_id();
 
-  if (warp == 8 && lane == 0) {
-    tma_prefetch_desc(&tm_main);
-    if (C::kRem) tma_prefetch_desc(&tm_rem);
+  if (warp == kTmaWarp && lane == 0) {
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_kv);
+    if (C::kRem) {
+      tma_prefetch_desc(&tm_q_rem);
+      tma_prefetch_desc(&tm_kv_rem);
+    }
     mbar_init(q_full, 1);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&v_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
-    for (int t = 0; t < 2; ++t) {
+    for (int t = 0; t < NQ; ++t) {
       mbar_init(&s_full[t], 1);
       mbar_init(&s_free[t], 4);  // one arrive per softmax warp
       mbar_init(&p_full[t], 4);
@@ -140,7 +150,7 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_main, const __grid_constant__
     }
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc<512>(tmem_slot);
+  if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -148,39 +158,41 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_main, const __grid_constant__
 
   auto tile_ptr = [&](int off) { return smem + off; };
 
-  if (warp == 8) {
+  if (warp == kTmaWarp) {
     // ---------------------------------------------------------------- TMA producer
     if (elect_one()) {
-      mbar_arrive_expect_tx(q_full, n_qt * C::kTileBytes);
+      mbar_arrive_expect_tx(q_full, n_qt * C::kQBytes);
       for (int t = 0; t < n_qt; ++t) {
-        uint8_t* q = tile_ptr(C::kQOff + t * C::kTileBytes);
-        tma_load_2d(&tm_main, q_full, q, col_q, s_begin + q0 + t * kTcBQ);
-        if (C::kRem) tma_load_2d(&tm_rem, q_full, q + C::kMainBytes, col_q + 64, s_begin + q0 + t * kTcBQ);
+        uint8_t* q = tile_ptr(C::kQOff + t * C::kQBytes);
+        tma_load_2d(&tm_q, q_full, q, col_q, s_begin + q0 + t * kTcBQ);
+        if (C::kRem) tma_load_2d(&tm_q_rem, q_full, q + C::kQMain, col_q + 64, s_begin + q0 + t * kTcBQ);
       }
       for (int j = 0; j < nkv; ++j) {
         const int st = j % C::STAGES;
         const uint32_t ph = (j / C::STAGES) & 1;
         mbar_wait(&kv_empty[st], ph ^ 1);
         uint8_t* kt = tile_ptr(C::kKVOff + st * C::kStageBytes);
-        uint8_t* vt = kt + C::kTileBytes;
-        const int row = s_begin + j * kTcBKV;
-        mbar_arrive_expect_tx(&k_full[st], C::kTileBytes);
-        tma_load_2d(&tm_main, &k_full[st], kt, col_k, row);
-        if (C::kRem) tma_load_2d(&tm_rem, &k_full[st], kt + C::kMainBytes, col_k + 64, row);
-        mbar_arrive_expect_tx(&v_full[st], C::kTileBytes);
-        tma_load_2d(&tm_main, &v_full[st], vt, col_v, row);
-        if (C::kRem) tma_load_2d(&tm_rem, &v_full[st], vt + C::kMainBytes, col_v + 64, row);
+        uint8_t* vt = kt + C::kKVBytes;
+        const int row = s_begin + j * BKV;
+        mbar_arrive_expect_tx(&k_full[st], C::kKVBytes);
+        tma_load_2d(&tm_kv, &k_full[st], kt, col_k, row);
+        if (C::kRem) tma_load_2d(&tm_kv_rem, &k_full[st], kt + C::kKVMain, col_k + 64, row);
+        mbar_arrive_expect_tx(&v_full[st], C::kKVBytes);
+        tma_load_2d(&tm_kv, &v_full[st], vt, col_v, row);
+        if (C::kRem) tma_load_2d(&tm_kv_rem, &v_full[st], vt + C::kKVMain, col_v + 64, row);
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == kMmaWarp) {
     // ---------------------------------------------------------------- MMA issuer
     // Whole warp runs the schedule (descriptors stay in uniform registers); one elected lane
-    // issues.  Per KV tile j: S0(j), S1(j) (each as soon as softmax_t released S_t), then
-    // PV0(j-1), PV1(j-1).
+    // issues.  Per KV tile j: S_t(j) for every tile (each as soon as softmax_t released S_t),
+    // then PV_t(j-1).
     {
-      constexpr uint32_t idesc_s = umma_idesc_bf16_f32(kTcBQ, kTcBKV);
+      constexpr uint32_t idesc_s = umma_idesc_bf16_f32(kTcBQ, BKV);
       constexpr uint32_t idesc_pv_main = umma_idesc_bf16_f32(kTcBQ, 64) | (1u << 16);  // B (V) MN-major
       constexpr uint32_t idesc_pv_rem = umma_idesc_bf16_f32(kTcBQ, 16) | (1u << 16);
+      // V as the MN-major B operand: 8-row K groups at 128 B (main) / 32 B (rem) per row
+      constexpr uint32_t kVStepMain = (16 * 128) >> 4, kVStepRem = (16 * 32) >> 4;  // desc units per k-step
       mbar_wait(q_full, 0);
       tc_fence_after();
       for (int j = 0; j <= nkv; ++j) {
@@ -197,46 +209,46 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_main, const __grid_constant__
               mbar_wait(&s_free[t], (j - 1) & 1);  // softmax has S_t(j-1) in registers
               tc_fence_after();
             }
-            const uint32_t s_tm = tmem + t * 128;
-            const uint32_t q_addr = smem_u32(tile_ptr(C::kQOff + t * C::kTileBytes));
+            const uint32_t s_tm = tmem + t * BKV;
+            const uint32_t q_addr = smem_u32(tile_ptr(C::kQOff + t * C::kQBytes));
             const uint64_t qd = umma_desc_sw128_kmajor(q_addr);
             if (elect_one()) {
 #pragma unroll
               for (int k = 0; k < 4; ++k) umma_bf16_ss(s_tm, qd + 2 * k, kd + 2 * k, idesc_s, k > 0);
               if (C::kRem)
-                umma_bf16_ss(s_tm, umma_desc_sw32_kmajor(q_addr + C::kMainBytes),
-                             umma_desc_sw32_kmajor(k_addr + C::kMainBytes), idesc_s, 1u);
+                umma_bf16_ss(s_tm, umma_desc_sw32_kmajor(q_addr + C::kQMain),
+                             umma_desc_sw32_kmajor(k_addr + C::kKVMain), idesc_s, 1u);
               umma_commit(&s_full[t]);
             }
             __syncwarp();
-            TR(2, j, 1 + t)
+            if (t < 2) { TR(2, j, 1 + t) }
           }
         }
         if (j > 0) {
           mbar_wait(&v_full[pst], ((j - 1) / C::STAGES) & 1);
           tc_fence_after();
-          const uint32_t v_addr = smem_u32(tile_ptr(C::kKVOff + pst * C::kStageBytes + C::kTileBytes));
-          const uint64_t vd_main = umma_desc_sw128_kmajor(v_addr);                // MN-major, SBO 1024
-          const uint64_t vd_rem = umma_desc_sw32_kmajor(v_addr + C::kMainBytes);  // MN-major, SBO 256
+          const uint32_t v_addr = smem_u32(tile_ptr(C::kKVOff + pst * C::kStageBytes + C::kKVBytes));
+          const uint64_t vd_main = umma_desc_sw128_kmajor(v_addr);                 // MN-major, SBO 1024
+          const uint64_t vd_rem = umma_desc_sw32_kmajor(v_addr + C::kKVMain);     // MN-major, SBO 256
           for (int t = 0; t < n_qt; ++t) {
             // O_t += P_t(j-1) V(j-1); P K-major (128B swizzle) in smem, V MN-major in smem
             mbar_wait(&p_full[t], (j - 1) & 1);
             tc_fence_after();
-            TR(2, j - 1, 3 + t)
-            const uint32_t o_tm = tmem + 256 + t * 128;
+            if (t < 2) { TR(2, j - 1, 3 + t) }
+            const uint32_t o_tm = tmem + C::kOBase + t * C::kOStride;
             const uint64_t pd0 = umma_desc_sw128_kmajor(smem_u32(tile_ptr(C::kPOff + t * C::kPBytes)));
             if (elect_one()) {
 #pragma unroll
-              for (int k = 0; k < kTcBKV / 16; ++k) {
+              for (int k = 0; k < BKV / 16; ++k) {
                 const uint32_t acc = (j > 1 || k > 0) ? 1u : 0u;
-                const uint64_t pd = pd0 + (k >> 2) * ((C::kPBytes / 2) >> 4) + 2 * (k & 3);
-                umma_bf16_ss(o_tm, pd, vd_main + (2048 >> 4) * k, idesc_pv_main, acc);
-                if (C::kRem) umma_bf16_ss(o_tm + 64, pd, vd_rem + (512 >> 4) * k, idesc_pv_rem, acc);
+                const uint64_t pd = pd0 + (k >> 2) * (C::kPBlock >> 4) + 2 * (k & 3);
+                umma_bf16_ss(o_tm, pd, vd_main + kVStepMain * k, idesc_pv_main, acc);
+                if (C::kRem) umma_bf16_ss(o_tm + 64, pd, vd_rem + kVStepRem * k, idesc_pv_rem, acc);
               }
               umma_commit(&pv_done[t]);
             }
             __syncwarp();
-            TR(2, j - 1, 5 + t)
+            if (t < 2) { TR(2, j - 1, 5 + t) }
           }
           if (elect_one()) umma_commit(&kv_empty[pst]);
           __syncwarp();
@@ -248,19 +260,19 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_main, const __grid_constant__
     const int t = warp >> 2;                 // query tile
     const uint32_t q4 = warp & 3;            // lane quarter
     const uint32_t lane_base = (q4 * 32u) << 16;
-    const uint32_t s_tm = tmem + t * 128 + lane_base;
-    const uint32_t o_tm = tmem + 256 + t * 128 + lane_base;
+    const uint32_t s_tm = tmem + t * BKV + lane_base;
+    const uint32_t o_tm = tmem + C::kOBase + t * C::kOStride + lane_base;
     const int row = q0 + t * kTcBQ + q4 * 32 + lane;  // query row within the sequence
     if (t < n_qt) {
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < nkv; ++j) {
-        if (q4 == 0 && lane == 0) { TR(t, j, 0) }
+        if (q4 == 0 && lane == 0 && t < 2) { TR(t, j, 0) }
         mbar_wait(&s_full[t], j & 1);
-        if (q4 == 0 && lane == 0) { TR(t, j, 1) }
+        if (q4 == 0 && lane == 0 && t < 2) { TR(t, j, 1) }
         tc_fence_after();
-        uint32_t r[128];
+        uint32_t r[BKV];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < BKV / 32; ++c) {
           uint32_t (&rc)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[32 * c]);
           tmem_ld_32x32b_x32(s_tm + 32 * c, rc);
         }
@@ -268,18 +280,18 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_main, const __grid_constant__
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_free[t]);  // TMEM S_t may now be overwritten by S_t(j+1)
-        if (q4 == 0 && lane == 0) { TR(t, j, 2) }
-        const int valid = len - j * kTcBKV;  // keys of this tile inside the sequence
-        if (valid < kTcBKV) {                 // last tile only (uniform branch)
+        if (q4 == 0 && lane == 0 && t < 2) { TR(t, j, 2) }
+        const int valid = len - j * BKV;  // keys of this tile inside the sequence
+        if (valid < BKV) {                // last tile only (uniform branch)
 #pragma unroll
-          for (int i = 0; i < 128; ++i)
+          for (int i = 0; i < BKV; ++i)
             if (i >= valid) r[i] = __float_as_uint(-INFINITY);
         }
         float mx;
         {
           float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-          for (int i = 0; i < 128; i += 8)
+          for (int i = 0; i < BKV; i += 8)
 #pragma unroll
             for (int u = 0; u < 4; ++u) m4[u] = fmax3(m4[u], __uint_as_float(r[i + 2 * u]), __uint_as_float(r[i + 2 * u + 1]));
           mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2;
@@ -305,13 +317,13 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_main, const __grid_constant__
           tmem_st_wait();
         }
         m_used = m_new;
-        // p = 2^(s*scale - m): half of the pairs on the FMA pipe (polynomial), half on MUFU
+        // p = 2^(s*scale - m): MMK_POLY8 of every 8 pairs on the FMA pipe (polynomial), the rest on MUFU
         const float2 sc2 = make_float2(scale_log2, scale_log2);
         const float2 nm2 = make_float2(-m_new, -m_new);
         float2 sa = make_float2(0.f, 0.f), sb = make_float2(0.f, 0.f);
-        uint32_t p[64];
+        uint32_t p[BKV / 2];
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
+        for (int i = 0; i < BKV / 2; ++i) {
           const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), sc2, nm2);
           float2 e;
           if ((i & 7) < MMK_POLY8) {
@@ -324,17 +336,17 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_main, const __grid_constant__
           p[i] = pack_bf16x2(e.x, e.y);
         }
         const float sum = (sa.x + sa.y) + (sb.x + sb.y);
-        if (q4 == 0 && lane == 0) { TR(t, j, 3) }
+        if (q4 == 0 && lane == 0 && t < 2) { TR(t, j, 3) }
         l = l * corr + sum;
         // P_t(j) -> smem (the PV MMA of tile j-1 must have finished reading the buffer)
         if (j > 0) mbar_wait(&pv_done[t], (j - 1) & 1);
-        if (q4 == 0 && lane == 0) { TR(t, j, 4) }
+        if (q4 == 0 && lane == 0 && t < 2) { TR(t, j, 4) }
         {
           const int r_in = q4 * 32 + lane;  // row of the 128-row tile
           uint8_t* pb = tile_ptr(C::kPOff + t * C::kPBytes);
 #pragma unroll
-          for (int c = 0; c < 16; ++c) {  // 16-byte chunk c = columns 8c..8c+7
-            uint8_t* dst = pb + (c >> 3) * (C::kPBytes / 2) + r_in * 128 + (((c & 7) ^ (r_in & 7)) << 4);
+          for (int c = 0; c < BKV / 8; ++c) {  // 16-byte chunk c = columns 8c..8c+7
+            uint8_t* dst = pb + (c >> 3) * C::kPBlock + r_in * 128 + (((c & 7) ^ (r_in & 7)) << 4);
             asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(dst)), "r"(p[4 * c]),
                          "r"(p[4 * c + 1]), "r"(p[4 * c + 2]), "r"(p[4 * c + 3])
                          : "memory");
@@ -344,7 +356,7 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_main, const __grid_constant__
         tc_fence_before();    // orders the O rescale (tcgen05.st) before the arrive
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[t]);
-        if (q4 == 0 && lane == 0) { TR(t, j, 5) }
+        if (q4 == 0 && lane == 0 && t < 2) { TR(t, j, 5) }
       }
       mbar_wait(&pv_done[t], (nkv - 1) & 1);
       tc_fence_after();
@@ -370,37 +382,46 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_main, const __grid_constant__
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 9) tmem_dealloc<512>(tmem);
+  if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
 }
 
-template <int HD>
-int launch_attn_tc(const void* qkv, void* out, const int32_t* cu, int n_seq, int max_s, int heads, float scale,
-                   int64_t total_rows, cudaStream_t stream) {
-  using C = TcAttnCfg<HD>;
+template <int HD, int BKV, int NQ>
+static int launch_attn_cfg(const void* qkv, void* out, const int32_t* cu, int n_seq, int max_s, int heads,
+                           float scale, int64_t total_rows, cudaStream_t stream) {
+  using C = TcAttnCfg<HD, BKV, NQ>;
   const uint64_t ld = 3ull * heads * HD;
-  CUtensorMap tm_main, tm_rem;
-  int rc = make_tmap_2d_bf16(&tm_main, qkv, ld, total_rows, ld, 64, 128, true);
+  const uint64_t dims[2] = {ld, static_cast<uint64_t>(total_rows)};
+  const uint64_t strides[1] = {ld * 2};
+  CUtensorMap tq, tqr, tkv, tkvr;
+  const uint32_t bq[2] = {64, kTcBQ}, bqr[2] = {16, kTcBQ}, bkv[2] = {64, BKV}, bkvr[2] = {16, BKV};
+  int rc = make_tmap_bf16(&tq, qkv, 2, dims, strides, bq, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!rc) rc = make_tmap_bf16(&tkv, qkv, 2, dims, strides, bkv, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!rc && C::kRem) rc = make_tmap_bf16(&tqr, qkv, 2, dims, strides, bqr, CU_TENSOR_MAP_SWIZZLE_32B);
+  if (!rc && C::kRem) rc = make_tmap_bf16(&tkvr, qkv, 2, dims, strides, bkvr, CU_TENSOR_MAP_SWIZZLE_32B);
   if (rc) return rc;
-  if (C::kRem) {
-    const uint64_t dims[2] = {ld, static_cast<uint64_t>(total_rows)};
-    const uint64_t strides[1] = {ld * 2};
-    const uint32_t box[2] = {16, 128};
-    rc = make_tmap_bf16(&tm_rem, qkv, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_32B);
-    if (rc) return rc;
-  } else {
-    tm_rem = tm_main;
-  }
+  if (!C::kRem) { tqr = tq; tkvr = tkv; }
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_tc<HD, BKV, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::kSmem);
     if (e != cudaSuccess) return set_cuda_error(e, "attention_tc: cudaFuncSetAttribute");
     attr = true;
   }
-  dim3 grid((max_s + 2 * kTcBQ - 1) / (2 * kTcBQ), n_seq, heads);
-  attn_fwd_tc<HD><<<grid, kTcThreads, C::kSmem, stream>>>(tm_main, tm_rem, reinterpret_cast<__nv_bfloat16*>(out), cu,
-                                                          heads, scale * 1.4426950408889634f);
+  dim3 grid((max_s + NQ * kTcBQ - 1) / (NQ * kTcBQ), n_seq, heads);
+  attn_fwd_tc<HD, BKV, NQ><<<grid, C::kThreads, C::kSmem, stream>>>(
+      tq, tqr, tkv, tkvr, reinterpret_cast<__nv_bfloat16*>(out), cu, heads, scale * 1.4426950408889634f);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "attention_tc: launch");
+}
+
+// Tile configuration per head_dim (measured on B200, profiles/r01_attention.md): hd 80 keeps
+// two 128-row query tiles with 128-key tiles (S 2x128 + O 2x128 TMEM columns); hd 64 (CLIP) runs
+// three query tiles with 64-key tiles (more softmax warps per SMSP, 121 registers, no spills).
+template <int HD>
+int launch_attn_tc(const void* qkv, void* out, const int32_t* cu, int n_seq, int max_s, int heads, float scale,
+                   int64_t total_rows, cudaStream_t stream) {
+  if (HD == 64) return launch_attn_cfg<HD, 64, 3>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, stream);
+  return launch_attn_cfg<HD, 128, 2>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, stream);
 }
 
 template int launch_attn_tc<64>(const void*, void*, const int32_t*, int, int, int, float, int64_t, cudaStream_t);
