@@ -420,8 +420,8 @@ static int launch_attn_cfg(const void* qkv, void* out, const int32_t* cu, int n_
 template <int HD>
 int launch_attn_tc(const void* qkv, void* out, const int32_t* cu, int n_seq, int max_s, int heads, float scale,
                    int64_t total_rows, cudaStream_t stream) {
-  if (HD == 64) return launch_attn_cfg<HD, 64, 3>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, stream);
-  return launch_attn_cfg<HD, 128, 2>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, stream);
+  if constexpr (HD == 64) return launch_attn_cfg<HD, 64, 3>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, stream);
+  else return launch_attn_cfg<HD, 128, 2>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, stream);
 }
 
 template int launch_attn_tc<64>(const void*, void*, const int32_t*, int, int, int, float, int64_t, cudaStream_t);

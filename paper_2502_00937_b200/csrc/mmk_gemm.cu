@@ -339,7 +339,9 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer (both CTAs)
-    const uint64_t pol_a = l2_policy_evict_first();
+    // A tiles are re-read by the N/256 clusters working on the same M block (normal policy);
+    // weights are re-read by every M block (keep in L2)
+    const uint64_t pol_a = l2_policy_evict_normal();
     const uint64_t pol_b = l2_policy_evict_last();
     int stage = 0;
     uint32_t phase = 0;
