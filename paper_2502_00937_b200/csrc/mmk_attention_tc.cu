@@ -116,7 +116,7 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
   uint64_t* pv_done = p_full + NQ;             // [NQ] MMA -> softmax: PV_t retired
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + NQ);
 
-  const int seq = blockIdx.y, head = blockIdx.z;
+  const int head = blockIdx.y, seq = blockIdx.z;  // heads of one image adjacent: K/V lines shared in L2
   const int s_begin = cu_seqlens[seq];
   const int len = cu_seqlens[seq + 1] - s_begin;
   const int q0 = blockIdx.x * NQ * kTcBQ;
@@ -407,7 +407,7 @@ static int launch_attn_cfg(const void* qkv, void* out, const int32_t* cu, int n_
     if (e != cudaSuccess) return set_cuda_error(e, "attention_tc: cudaFuncSetAttribute");
     attr = true;
   }
-  dim3 grid((max_s + NQ * kTcBQ - 1) / (NQ * kTcBQ), n_seq, heads);
+  dim3 grid((max_s + NQ * kTcBQ - 1) / (NQ * kTcBQ), heads, n_seq);
   attn_fwd_tc<HD, BKV, NQ><<<grid, C::kThreads, C::kSmem, stream>>>(
       tq, tqr, tkv, tkvr, reinterpret_cast<__nv_bfloat16*>(out), cu, heads, scale * 1.4426950408889634f);
   cudaError_t e = cudaGetLastError();
