@@ -38,26 +38,31 @@ __device__ long long g_attn_trace[3][64][8];
 constexpr int kTcBQ = 128;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
-template <int HD, int BKV, int NQ>
+template <int HD, int BKV, int NQ, bool PT>
 struct TcAttnCfg {
   static constexpr bool kRem = (HD % 64) != 0;               // has a 16-wide remainder block
   static constexpr int kQMain = kTcBQ * 64 * 2;              // Q tile: 128 rows x 64 cols
   static constexpr int kQBytes = kQMain + (kRem ? kTcBQ * 16 * 2 : 0);
   static constexpr int kKVMain = BKV * 64 * 2;               // K or V tile: BKV rows x 64 cols
   static constexpr int kKVBytes = kKVMain + (kRem ? BKV * 16 * 2 : 0);
-  static constexpr int STAGES = BKV == 128 ? 3 : 4;
+  static constexpr int STAGES = PT ? 4 : (BKV == 128 ? 3 : 4);
   static constexpr int kQOff = 0;
   static constexpr int kKVOff = NQ * kQBytes;
   static constexpr int kStageBytes = 2 * kKVBytes;           // K then V
   static constexpr int kPOff = kKVOff + STAGES * kStageBytes;  // P_t: [BKV/64 blocks][128 rows][128 B]
   static constexpr int kPBlock = kTcBQ * 128;
-  static constexpr int kPBytes = (BKV / 64) * kPBlock;
+  static constexpr int kPBytes = PT ? 0 : (BKV / 64) * kPBlock;
   static constexpr int kBarOff = kPOff + NQ * kPBytes;
   static constexpr int kSmem = kBarOff + 256 + 1024;
   static constexpr int kThreads = 32 * (4 * NQ + 2);
   static constexpr int kOBase = NQ * BKV;                    // TMEM column of O_0
-  static constexpr int kOStride = (512 - NQ * BKV) / NQ >= 128 ? 128 : 96;
-  static_assert(kOBase + (NQ - 1) * kOStride + HD <= 512, "TMEM overflow");
+  static constexpr int kOStride = PT ? HD : ((512 - NQ * BKV) / NQ >= 128 ? 128 : 96);
+  static constexpr int kPTBase = kOBase + NQ * kOStride;     // PT: TMEM column of P_0 (bf16 pairs)
+  static constexpr int kPTBaseAligned = (kPTBase + 31) / 32 * 32;  // P_t at kPTBaseAligned + kPStride t
+  static constexpr int kPStride = (BKV / 2 + 31) / 32 * 32;
+  static_assert((PT ? kPTBaseAligned + (NQ - 1) * kPStride + BKV / 2 : kOBase + (NQ - 1) * kOStride + HD) <= 512,
+                "TMEM overflow");
+  static_assert(BKV % 16 == 0 && (PT || BKV % 64 == 0), "key tile");
   static_assert(kSmem <= 232448, "shared memory overflow");
 };
 
@@ -96,12 +101,12 @@ MMK_DEV float2 exp2_poly2(float2 x) {
   return e;
 }
 
-template <int HD, int BKV, int NQ>
+template <int HD, int BKV, int NQ, bool PT>
 __global__ void __maxnreg__(NQ == 2 ? 168 : 128)
 attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_q_rem,
             const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_kv_rem,
             __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ cu_seqlens, int heads, float scale_log2) {
-  using C = TcAttnCfg<HD, BKV, NQ>;
+  using C = TcAttnCfg<HD, BKV, NQ, PT>;
   constexpr int kTmaWarp = 4 * NQ, kMmaWarp = 4 * NQ + 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -236,14 +241,25 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
             tc_fence_after();
             if (t < 2) { TR(2, j - 1, 3 + t) }
             const uint32_t o_tm = tmem + C::kOBase + t * C::kOStride;
-            const uint64_t pd0 = umma_desc_sw128_kmajor(smem_u32(tile_ptr(C::kPOff + t * C::kPBytes)));
             if (elect_one()) {
+              if constexpr (PT) {
+                // P_t in TMEM (bf16 pairs, 8 columns per 16 keys): A operand read from tensor memory
+                const uint32_t p_tm = tmem + C::kPTBaseAligned + t * C::kPStride;
 #pragma unroll
-              for (int k = 0; k < BKV / 16; ++k) {
-                const uint32_t acc = (j > 1 || k > 0) ? 1u : 0u;
-                const uint64_t pd = pd0 + (k >> 2) * (C::kPBlock >> 4) + 2 * (k & 3);
-                umma_bf16_ss(o_tm, pd, vd_main + kVStepMain * k, idesc_pv_main, acc);
-                if (C::kRem) umma_bf16_ss(o_tm + 64, pd, vd_rem + kVStepRem * k, idesc_pv_rem, acc);
+                for (int k = 0; k < BKV / 16; ++k) {
+                  const uint32_t acc = (j > 1 || k > 0) ? 1u : 0u;
+                  umma_bf16_ts(o_tm, p_tm + 8 * k, vd_main + kVStepMain * k, idesc_pv_main, acc);
+                  if (C::kRem) umma_bf16_ts(o_tm + 64, p_tm + 8 * k, vd_rem + kVStepRem * k, idesc_pv_rem, acc);
+                }
+              } else {
+                const uint64_t pd0 = umma_desc_sw128_kmajor(smem_u32(tile_ptr(C::kPOff + t * C::kPBytes)));
+#pragma unroll
+                for (int k = 0; k < BKV / 16; ++k) {
+                  const uint32_t acc = (j > 1 || k > 0) ? 1u : 0u;
+                  const uint64_t pd = pd0 + (k >> 2) * (C::kPBlock >> 4) + 2 * (k & 3);
+                  umma_bf16_ss(o_tm, pd, vd_main + kVStepMain * k, idesc_pv_main, acc);
+                  if (C::kRem) umma_bf16_ss(o_tm + 64, pd, vd_rem + kVStepRem * k, idesc_pv_rem, acc);
+                }
               }
               umma_commit(&pv_done[t]);
             }
@@ -275,6 +291,10 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
         for (int c = 0; c < BKV / 32; ++c) {
           uint32_t (&rc)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[32 * c]);
           tmem_ld_32x32b_x32(s_tm + 32 * c, rc);
+        }
+        if constexpr (BKV % 32 != 0) {
+          uint32_t (&rc)[16] = *reinterpret_cast<uint32_t(*)[16]>(&r[BKV - 16]);
+          tmem_ld_32x32b_x16(s_tm + BKV - 16, rc);
         }
         tmem_ld_wait();
         tc_fence_before();
@@ -338,10 +358,21 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
         const float sum = (sa.x + sa.y) + (sb.x + sb.y);
         if (q4 == 0 && lane == 0 && t < 2) { TR(t, j, 3) }
         l = l * corr + sum;
-        // P_t(j) -> smem (the PV MMA of tile j-1 must have finished reading the buffer)
+        // P_t(j) -> smem / TMEM (the PV MMA of tile j-1 must have finished reading the buffer)
         if (j > 0) mbar_wait(&pv_done[t], (j - 1) & 1);
         if (q4 == 0 && lane == 0 && t < 2) { TR(t, j, 4) }
-        {
+        if constexpr (PT) {
+          tc_fence_after();
+          const uint32_t p_tm = tmem + C::kPTBaseAligned + t * C::kPStride + lane_base;
+#pragma unroll
+          for (int c = 0; c < BKV / 64; ++c)
+            tmem_st_32x32b_x32(p_tm + 32 * c, *reinterpret_cast<const uint32_t(*)[32]>(&p[32 * c]));
+          if constexpr ((BKV / 2) % 32 >= 16)
+            tmem_st_32x32b_x16(p_tm + (BKV / 64) * 32, *reinterpret_cast<const uint32_t(*)[16]>(&p[(BKV / 64) * 32]));
+          if constexpr ((BKV / 2) % 16 == 8)
+            tmem_st_32x32b_x8(p_tm + BKV / 2 - 8, *reinterpret_cast<const uint32_t(*)[8]>(&p[BKV / 2 - 8]));
+          tmem_st_wait();
+        } else {
           const int r_in = q4 * 32 + lane;  // row of the 128-row tile
           uint8_t* pb = tile_ptr(C::kPOff + t * C::kPBytes);
 #pragma unroll
@@ -351,9 +382,9 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
                          "r"(p[4 * c + 1]), "r"(p[4 * c + 2]), "r"(p[4 * c + 3])
                          : "memory");
           }
+          fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
         }
-        fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
-        tc_fence_before();    // orders the O rescale (tcgen05.st) before the arrive
+        tc_fence_before();    // orders the O rescale / P (tcgen05.st) before the arrive
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[t]);
         if (q4 == 0 && lane == 0 && t < 2) { TR(t, j, 5) }
@@ -385,10 +416,10 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
   if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
 }
 
-template <int HD, int BKV, int NQ>
+template <int HD, int BKV, int NQ, bool PT>
 static int launch_attn_cfg(const void* qkv, void* out, const int32_t* cu, int n_seq, int max_s, int heads,
                            float scale, int64_t total_rows, cudaStream_t stream) {
-  using C = TcAttnCfg<HD, BKV, NQ>;
+  using C = TcAttnCfg<HD, BKV, NQ, PT>;
   const uint64_t ld = 3ull * heads * HD;
   const uint64_t dims[2] = {ld, static_cast<uint64_t>(total_rows)};
   const uint64_t strides[1] = {ld * 2};
@@ -402,26 +433,27 @@ static int launch_attn_cfg(const void* qkv, void* out, const int32_t* cu, int n_
   if (!C::kRem) { tqr = tq; tkvr = tkv; }
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_tc<HD, BKV, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_tc<HD, BKV, NQ, PT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmem);
     if (e != cudaSuccess) return set_cuda_error(e, "attention_tc: cudaFuncSetAttribute");
     attr = true;
   }
   dim3 grid((max_s + NQ * kTcBQ - 1) / (NQ * kTcBQ), heads, n_seq);
-  attn_fwd_tc<HD, BKV, NQ><<<grid, C::kThreads, C::kSmem, stream>>>(
+  attn_fwd_tc<HD, BKV, NQ, PT><<<grid, C::kThreads, C::kSmem, stream>>>(
       tq, tqr, tkv, tkvr, reinterpret_cast<__nv_bfloat16*>(out), cu, heads, scale * 1.4426950408889634f);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "attention_tc: launch");
 }
 
-// Tile configuration per head_dim (measured on B200, profiles/r01_attention.md): hd 80 keeps
-// two 128-row query tiles with 128-key tiles (S 2x128 + O 2x128 TMEM columns); hd 64 (CLIP) runs
-// three query tiles with 64-key tiles (more softmax warps per SMSP, 121 registers, no spills).
+// Tile configuration per head_dim (measured on B200, profiles/r01_attention.md).  Both keep P in
+// TMEM (A operand of the PV MMA read from tensor memory), which needs S + O + P <= 512 columns:
+//   hd 80: 2 query tiles, 112-key tiles:  S 2x112 + O 2x80 + P 2x56 (aligned)  = 504 columns
+//   hd 64: 3 query tiles,  64-key tiles:  S 3x64  + O 3x64 + P 3x32           = 480 columns
 template <int HD>
 int launch_attn_tc(const void* qkv, void* out, const int32_t* cu, int n_seq, int max_s, int heads, float scale,
                    int64_t total_rows, cudaStream_t stream) {
-  if constexpr (HD == 64) return launch_attn_cfg<HD, 64, 3>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, stream);
-  else return launch_attn_cfg<HD, 128, 2>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, stream);
+  if constexpr (HD == 64) return launch_attn_cfg<HD, 64, 3, true>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, stream);
+  else return launch_attn_cfg<HD, 112, 2, true>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, stream);
 }
 
 template int launch_attn_tc<64>(const void*, void*, const int32_t*, int, int, int, float, int64_t, cudaStream_t);
