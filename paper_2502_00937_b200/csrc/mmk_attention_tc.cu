@@ -32,7 +32,7 @@ __device__ long long g_attn_trace[3][64][8];
 #endif
 
 #ifndef MMK_POLY8
-#define MMK_POLY8 3  // pairs out of every 8 whose exp2 runs as an FMA-pipe polynomial
+#define MMK_POLY8 2  // pairs out of every 8 whose exp2 runs as an FMA-pipe polynomial
 #endif
 
 constexpr int kTcBQ = 128;
