@@ -54,7 +54,7 @@ struct TcAttnCfg {
   static constexpr int kPBytes = PT ? 0 : (BKV / 64) * kPBlock;
   static constexpr int kBarOff = kPOff + NQ * kPBytes;
   static constexpr int kSmem = kBarOff + 256 + 1024;
-  static constexpr int kThreads = 32 * (4 * NQ + 2);
+  static constexpr int kThreads = 32 * (5 * NQ + 1);  // NQ softmax warpgroups, TMA warp, NQ MMA warps
   static constexpr int kOBase = NQ * BKV;                    // TMEM column of O_0
   static constexpr int kOStride = PT ? HD : ((512 - NQ * BKV) / NQ >= 128 ? 128 : 96);
   static constexpr int kPTBase = kOBase + NQ * kOStride;     // PT: TMEM column of P_0 (bf16 pairs)
@@ -107,7 +107,7 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
             const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_kv_rem,
             __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ cu_seqlens, int heads, float scale_log2) {
   using C = TcAttnCfg<HD, BKV, NQ, PT>;
-  constexpr int kTmaWarp = 4 * NQ, kMmaWarp = 4 * NQ + 1;
+  constexpr int kTmaWarp = 4 * NQ, kMmaWarp = 4 * NQ + 1;  // MMA warp of query tile t: kMmaWarp + t
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
@@ -145,7 +145,7 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&v_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
+      mbar_init(&kv_empty[s], n_qt);  // released by every tile's MMA warp
     }
     for (int t = 0; t < NQ; ++t) {
       mbar_init(&s_full[t], 1);
@@ -187,17 +187,23 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
         if (C::kRem) tma_load_2d(&tm_kv_rem, &v_full[st], vt + C::kKVMain, col_v + 64, row);
       }
     }
-  } else if (warp == kMmaWarp) {
-    // ---------------------------------------------------------------- MMA issuer
-    // Whole warp runs the schedule (descriptors stay in uniform registers); one elected lane
-    // issues.  Per KV tile j: S_t(j) for every tile (each as soon as softmax_t released S_t),
-    // then PV_t(j-1).
-    {
+  } else if (warp > kTmaWarp) {
+    // ---------------------------------------------------------------- MMA issuers
+    // One warp per query tile, so one tile's S never queues behind the other tile's PV in an
+    // issue order; the whole warp runs the schedule (descriptors stay in uniform registers) and
+    // one elected lane issues.  Per KV tile j: S_t(j) once softmax_t released S_t(j-1), then
+    // PV_t(j-1) once P_t(j-1) is written.
+    const int t = static_cast<int>(warp) - kMmaWarp;
+    if (t < n_qt) {
       constexpr uint32_t idesc_s = umma_idesc_bf16_f32(kTcBQ, BKV);
       constexpr uint32_t idesc_pv_main = umma_idesc_bf16_f32(kTcBQ, 64) | (1u << 16);  // B (V) MN-major
       constexpr uint32_t idesc_pv_rem = umma_idesc_bf16_f32(kTcBQ, 16) | (1u << 16);
       // V as the MN-major B operand: 8-row K groups at 128 B (main) / 32 B (rem) per row
       constexpr uint32_t kVStepMain = (16 * 128) >> 4, kVStepRem = (16 * 32) >> 4;  // desc units per k-step
+      const uint32_t s_tm = tmem + t * BKV;
+      const uint32_t o_tm = tmem + C::kOBase + t * C::kOStride;
+      const uint32_t q_addr = smem_u32(tile_ptr(C::kQOff + t * C::kQBytes));
+      const uint64_t qd = umma_desc_sw128_kmajor(q_addr);
       mbar_wait(q_full, 0);
       tc_fence_after();
       for (int j = 0; j <= nkv; ++j) {
@@ -205,69 +211,55 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
         const int pst = (j - 1 + C::STAGES) % C::STAGES;
         if (j < nkv) {
           mbar_wait(&k_full[st], (j / C::STAGES) & 1);
+          if (j > 0) mbar_wait(&s_free[t], (j - 1) & 1);  // softmax has S_t(j-1) in registers
           tc_fence_after();
-          TR(2, j, 0)
+          if (t < 2) { TR(2, j, 0) }
           const uint32_t k_addr = smem_u32(tile_ptr(C::kKVOff + st * C::kStageBytes));
           const uint64_t kd = umma_desc_sw128_kmajor(k_addr);
-          for (int t = 0; t < n_qt; ++t) {
-            if (j > 0) {
-              mbar_wait(&s_free[t], (j - 1) & 1);  // softmax has S_t(j-1) in registers
-              tc_fence_after();
-            }
-            const uint32_t s_tm = tmem + t * BKV;
-            const uint32_t q_addr = smem_u32(tile_ptr(C::kQOff + t * C::kQBytes));
-            const uint64_t qd = umma_desc_sw128_kmajor(q_addr);
-            if (elect_one()) {
+          if (elect_one()) {
 #pragma unroll
-              for (int k = 0; k < 4; ++k) umma_bf16_ss(s_tm, qd + 2 * k, kd + 2 * k, idesc_s, k > 0);
-              if (C::kRem)
-                umma_bf16_ss(s_tm, umma_desc_sw32_kmajor(q_addr + C::kQMain),
-                             umma_desc_sw32_kmajor(k_addr + C::kKVMain), idesc_s, 1u);
-              umma_commit(&s_full[t]);
-            }
-            __syncwarp();
-            if (t < 2) { TR(2, j, 1 + t) }
+            for (int k = 0; k < 4; ++k) umma_bf16_ss(s_tm, qd + 2 * k, kd + 2 * k, idesc_s, k > 0);
+            if (C::kRem)
+              umma_bf16_ss(s_tm, umma_desc_sw32_kmajor(q_addr + C::kQMain),
+                           umma_desc_sw32_kmajor(k_addr + C::kKVMain), idesc_s, 1u);
+            umma_commit(&s_full[t]);
           }
+          __syncwarp();
+          if (t < 2) { TR(2, j, 1 + t) }
         }
         if (j > 0) {
           mbar_wait(&v_full[pst], ((j - 1) / C::STAGES) & 1);
+          mbar_wait(&p_full[t], (j - 1) & 1);
           tc_fence_after();
+          if (t < 2) { TR(2, j - 1, 3 + t) }
           const uint32_t v_addr = smem_u32(tile_ptr(C::kKVOff + pst * C::kStageBytes + C::kKVBytes));
           const uint64_t vd_main = umma_desc_sw128_kmajor(v_addr);                 // MN-major, SBO 1024
           const uint64_t vd_rem = umma_desc_sw32_kmajor(v_addr + C::kKVMain);     // MN-major, SBO 256
-          for (int t = 0; t < n_qt; ++t) {
-            // O_t += P_t(j-1) V(j-1); P K-major (128B swizzle) in smem, V MN-major in smem
-            mbar_wait(&p_full[t], (j - 1) & 1);
-            tc_fence_after();
-            if (t < 2) { TR(2, j - 1, 3 + t) }
-            const uint32_t o_tm = tmem + C::kOBase + t * C::kOStride;
-            if (elect_one()) {
-              if constexpr (PT) {
-                // P_t in TMEM (bf16 pairs, 8 columns per 16 keys): A operand read from tensor memory
-                const uint32_t p_tm = tmem + C::kPTBaseAligned + t * C::kPStride;
+          if (elect_one()) {
+            if constexpr (PT) {
+              // P_t in TMEM (bf16 pairs, 8 columns per 16 keys): A operand read from tensor memory
+              const uint32_t p_tm = tmem + C::kPTBaseAligned + t * C::kPStride;
 #pragma unroll
-                for (int k = 0; k < BKV / 16; ++k) {
-                  const uint32_t acc = (j > 1 || k > 0) ? 1u : 0u;
-                  umma_bf16_ts(o_tm, p_tm + 8 * k, vd_main + kVStepMain * k, idesc_pv_main, acc);
-                  if (C::kRem) umma_bf16_ts(o_tm + 64, p_tm + 8 * k, vd_rem + kVStepRem * k, idesc_pv_rem, acc);
-                }
-              } else {
-                const uint64_t pd0 = umma_desc_sw128_kmajor(smem_u32(tile_ptr(C::kPOff + t * C::kPBytes)));
-#pragma unroll
-                for (int k = 0; k < BKV / 16; ++k) {
-                  const uint32_t acc = (j > 1 || k > 0) ? 1u : 0u;
-                  const uint64_t pd = pd0 + (k >> 2) * (C::kPBlock >> 4) + 2 * (k & 3);
-                  umma_bf16_ss(o_tm, pd, vd_main + kVStepMain * k, idesc_pv_main, acc);
-                  if (C::kRem) umma_bf16_ss(o_tm + 64, pd, vd_rem + kVStepRem * k, idesc_pv_rem, acc);
-                }
+              for (int k = 0; k < BKV / 16; ++k) {
+                const uint32_t acc = (j > 1 || k > 0) ? 1u : 0u;
+                umma_bf16_ts(o_tm, p_tm + 8 * k, vd_main + kVStepMain * k, idesc_pv_main, acc);
+                if (C::kRem) umma_bf16_ts(o_tm + 64, p_tm + 8 * k, vd_rem + kVStepRem * k, idesc_pv_rem, acc);
               }
-              umma_commit(&pv_done[t]);
+            } else {
+              const uint64_t pd0 = umma_desc_sw128_kmajor(smem_u32(tile_ptr(C::kPOff + t * C::kPBytes)));
+#pragma unroll
+              for (int k = 0; k < BKV / 16; ++k) {
+                const uint32_t acc = (j > 1 || k > 0) ? 1u : 0u;
+                const uint64_t pd = pd0 + (k >> 2) * (C::kPBlock >> 4) + 2 * (k & 3);
+                umma_bf16_ss(o_tm, pd, vd_main + kVStepMain * k, idesc_pv_main, acc);
+                if (C::kRem) umma_bf16_ss(o_tm + 64, pd, vd_rem + kVStepRem * k, idesc_pv_rem, acc);
+              }
             }
-            __syncwarp();
-            if (t < 2) { TR(2, j - 1, 5 + t) }
+            umma_commit(&pv_done[t]);
+            umma_commit(&kv_empty[pst]);  // this tile is done with K(j-1), V(j-1)
           }
-          if (elect_one()) umma_commit(&kv_empty[pst]);
           __syncwarp();
+          if (t < 2) { TR(2, j - 1, 5 + t) }
         }
       }
     }
