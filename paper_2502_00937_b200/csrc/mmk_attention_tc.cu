@@ -4,12 +4,13 @@
 // CTA = NQ 128-row query tiles of one (sequence, head), KV tiles of BKV keys; warp roles:
 //   warps 4t..4t+3   softmax warpgroup t (query tile t, TMEM lanes 0-127 = rows)
 //   warp 4*NQ        TMA producer (Q once; K/V tiles into a STAGES-deep ring)
-//   warp 4*NQ + 1    MMA issuer (warp-uniform, one elected lane) + TMEM allocator
+//   warps 4*NQ+1..   MMA issuer of query tile t (warp-uniform, one elected lane); the first
+//                    also allocates TMEM
 // TMEM (512 columns): S_t at [t*BKV, (t+1)*BKV), O_t after them (hd columns each).  A softmax
 // warpgroup releases its S buffer as soon as the scores are in registers (s_free), so the MMA
 // warp issues S_t(j+1) = Q_t K(j+1)^T while the exponentials of tile j are still being
-// computed; P (bf16) goes to a 128B-swizzled shared-memory tile (K-major A operand of the PV
-// MMA).  Per KV tile j the MMA warp issues S_0..S_{NQ-1}(j), then PV_0..PV_{NQ-1}(j-1).
+// computed; P (bf16 pairs) is written back to TMEM and read from there as the A operand of the
+// PV MMA.  One MMA-issuer warp per query tile issues S_t(j) then PV_t(j-1).
 // Online softmax in base 2 with a lazily updated running max (rescale O only when the row max
 // grows by more than 2^8), so O is rarely touched.
 //
@@ -38,31 +39,25 @@ __device__ long long g_attn_trace[3][64][8];
 constexpr int kTcBQ = 128;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
-template <int HD, int BKV, int NQ, bool PT>
+template <int HD, int BKV, int NQ>
 struct TcAttnCfg {
   static constexpr bool kRem = (HD % 64) != 0;               // has a 16-wide remainder block
   static constexpr int kQMain = kTcBQ * 64 * 2;              // Q tile: 128 rows x 64 cols
   static constexpr int kQBytes = kQMain + (kRem ? kTcBQ * 16 * 2 : 0);
   static constexpr int kKVMain = BKV * 64 * 2;               // K or V tile: BKV rows x 64 cols
   static constexpr int kKVBytes = kKVMain + (kRem ? BKV * 16 * 2 : 0);
-  static constexpr int STAGES = PT ? 4 : (BKV == 128 ? 3 : 4);
+  static constexpr int STAGES = 4;
   static constexpr int kQOff = 0;
   static constexpr int kKVOff = NQ * kQBytes;
   static constexpr int kStageBytes = 2 * kKVBytes;           // K then V
-  static constexpr int kPOff = kKVOff + STAGES * kStageBytes;  // P_t: [BKV/64 blocks][128 rows][128 B]
-  static constexpr int kPBlock = kTcBQ * 128;
-  static constexpr int kPBytes = PT ? 0 : (BKV / 64) * kPBlock;
-  static constexpr int kBarOff = kPOff + NQ * kPBytes;
+  static constexpr int kBarOff = kKVOff + STAGES * kStageBytes;
   static constexpr int kSmem = kBarOff + 256 + 1024;
   static constexpr int kThreads = 32 * (5 * NQ + 1);  // NQ softmax warpgroups, TMA warp, NQ MMA warps
-  static constexpr int kOBase = NQ * BKV;                    // TMEM column of O_0
-  static constexpr int kOStride = PT ? HD : ((512 - NQ * BKV) / NQ >= 128 ? 128 : 96);
-  static constexpr int kPTBase = kOBase + NQ * kOStride;     // PT: TMEM column of P_0 (bf16 pairs)
-  static constexpr int kPTBaseAligned = (kPTBase + 31) / 32 * 32;  // P_t at kPTBaseAligned + kPStride t
+  static constexpr int kOBase = NQ * BKV;                    // TMEM column of O_0 (O_t: + t*HD)
+  static constexpr int kPBase = (kOBase + NQ * HD + 31) / 32 * 32;  // P_t (bf16 pairs): + t*kPStride
   static constexpr int kPStride = (BKV / 2 + 31) / 32 * 32;
-  static_assert((PT ? kPTBaseAligned + (NQ - 1) * kPStride + BKV / 2 : kOBase + (NQ - 1) * kOStride + HD) <= 512,
-                "TMEM overflow");
-  static_assert(BKV % 16 == 0 && (PT || BKV % 64 == 0), "key tile");
+  static_assert(kPBase + (NQ - 1) * kPStride + BKV / 2 <= 512, "TMEM overflow: S + O + P > 512 columns");
+  static_assert(BKV % 16 == 0, "key tile");
   static_assert(kSmem <= 232448, "shared memory overflow");
 };
 
@@ -101,12 +96,12 @@ MMK_DEV float2 exp2_poly2(float2 x) {
   return e;
 }
 
-template <int HD, int BKV, int NQ, bool PT>
+template <int HD, int BKV, int NQ>
 __global__ void __maxnreg__(NQ == 2 ? 168 : 128)
 attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_q_rem,
             const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_kv_rem,
             __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ cu_seqlens, int heads, float scale_log2) {
-  using C = TcAttnCfg<HD, BKV, NQ, PT>;
+  using C = TcAttnCfg<HD, BKV, NQ>;
   constexpr int kTmaWarp = 4 * NQ, kMmaWarp = 4 * NQ + 1;  // MMA warp of query tile t: kMmaWarp + t
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -201,7 +196,7 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
       // V as the MN-major B operand: 8-row K groups at 128 B (main) / 32 B (rem) per row
       constexpr uint32_t kVStepMain = (16 * 128) >> 4, kVStepRem = (16 * 32) >> 4;  // desc units per k-step
       const uint32_t s_tm = tmem + t * BKV;
-      const uint32_t o_tm = tmem + C::kOBase + t * C::kOStride;
+      const uint32_t o_tm = tmem + C::kOBase + t * HD;
       const uint32_t q_addr = smem_u32(tile_ptr(C::kQOff + t * C::kQBytes));
       const uint64_t qd = umma_desc_sw128_kmajor(q_addr);
       mbar_wait(q_full, 0);
@@ -236,24 +231,13 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
           const uint64_t vd_main = umma_desc_sw128_kmajor(v_addr);                 // MN-major, SBO 1024
           const uint64_t vd_rem = umma_desc_sw32_kmajor(v_addr + C::kKVMain);     // MN-major, SBO 256
           if (elect_one()) {
-            if constexpr (PT) {
-              // P_t in TMEM (bf16 pairs, 8 columns per 16 keys): A operand read from tensor memory
-              const uint32_t p_tm = tmem + C::kPTBaseAligned + t * C::kPStride;
+            // P_t in TMEM (bf16 pairs, 8 columns per 16 keys): A operand read from tensor memory
+            const uint32_t p_tm = tmem + C::kPBase + t * C::kPStride;
 #pragma unroll
-              for (int k = 0; k < BKV / 16; ++k) {
-                const uint32_t acc = (j > 1 || k > 0) ? 1u : 0u;
-                umma_bf16_ts(o_tm, p_tm + 8 * k, vd_main + kVStepMain * k, idesc_pv_main, acc);
-                if (C::kRem) umma_bf16_ts(o_tm + 64, p_tm + 8 * k, vd_rem + kVStepRem * k, idesc_pv_rem, acc);
-              }
-            } else {
-              const uint64_t pd0 = umma_desc_sw128_kmajor(smem_u32(tile_ptr(C::kPOff + t * C::kPBytes)));
-#pragma unroll
-              for (int k = 0; k < BKV / 16; ++k) {
-                const uint32_t acc = (j > 1 || k > 0) ? 1u : 0u;
-                const uint64_t pd = pd0 + (k >> 2) * (C::kPBlock >> 4) + 2 * (k & 3);
-                umma_bf16_ss(o_tm, pd, vd_main + kVStepMain * k, idesc_pv_main, acc);
-                if (C::kRem) umma_bf16_ss(o_tm + 64, pd, vd_rem + kVStepRem * k, idesc_pv_rem, acc);
-              }
+            for (int k = 0; k < BKV / 16; ++k) {
+              const uint32_t acc = (j > 1 || k > 0) ? 1u : 0u;
+              umma_bf16_ts(o_tm, p_tm + 8 * k, vd_main + kVStepMain * k, idesc_pv_main, acc);
+              if (C::kRem) umma_bf16_ts(o_tm + 64, p_tm + 8 * k, vd_rem + kVStepRem * k, idesc_pv_rem, acc);
             }
             umma_commit(&pv_done[t]);
             umma_commit(&kv_empty[pst]);  // this tile is done with K(j-1), V(j-1)
@@ -269,7 +253,7 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
     const uint32_t q4 = warp & 3;            // lane quarter
     const uint32_t lane_base = (q4 * 32u) << 16;
     const uint32_t s_tm = tmem + t * BKV + lane_base;
-    const uint32_t o_tm = tmem + C::kOBase + t * C::kOStride + lane_base;
+    const uint32_t o_tm = tmem + C::kOBase + t * HD + lane_base;
     const int row = q0 + t * kTcBQ + q4 * 32 + lane;  // query row within the sequence
     if (t < n_qt) {
       float m_used = -INFINITY, l = 0.f;
@@ -350,12 +334,12 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
         const float sum = (sa.x + sa.y) + (sb.x + sb.y);
         if (q4 == 0 && lane == 0 && t < 2) { TR(t, j, 3) }
         l = l * corr + sum;
-        // P_t(j) -> smem / TMEM (the PV MMA of tile j-1 must have finished reading the buffer)
+        // P_t(j) -> TMEM (the PV MMA of tile j-1 must have finished reading the buffer)
         if (j > 0) mbar_wait(&pv_done[t], (j - 1) & 1);
         if (q4 == 0 && lane == 0 && t < 2) { TR(t, j, 4) }
-        if constexpr (PT) {
+        {
           tc_fence_after();
-          const uint32_t p_tm = tmem + C::kPTBaseAligned + t * C::kPStride + lane_base;
+          const uint32_t p_tm = tmem + C::kPBase + t * C::kPStride + lane_base;
 #pragma unroll
           for (int c = 0; c < BKV / 64; ++c)
             tmem_st_32x32b_x32(p_tm + 32 * c, *reinterpret_cast<const uint32_t(*)[32]>(&p[32 * c]));
@@ -364,17 +348,6 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
           if constexpr ((BKV / 2) % 16 == 8)
             tmem_st_32x32b_x8(p_tm + BKV / 2 - 8, *reinterpret_cast<const uint32_t(*)[8]>(&p[BKV / 2 - 8]));
           tmem_st_wait();
-        } else {
-          const int r_in = q4 * 32 + lane;  // row of the 128-row tile
-          uint8_t* pb = tile_ptr(C::kPOff + t * C::kPBytes);
-#pragma unroll
-          for (int c = 0; c < BKV / 8; ++c) {  // 16-byte chunk c = columns 8c..8c+7
-            uint8_t* dst = pb + (c >> 3) * C::kPBlock + r_in * 128 + (((c & 7) ^ (r_in & 7)) << 4);
-            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(dst)), "r"(p[4 * c]),
-                         "r"(p[4 * c + 1]), "r"(p[4 * c + 2]), "r"(p[4 * c + 3])
-                         : "memory");
-          }
-          fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
         }
         tc_fence_before();    // orders the O rescale / P (tcgen05.st) before the arrive
         __syncwarp();
@@ -408,10 +381,10 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
   if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
 }
 
-template <int HD, int BKV, int NQ, bool PT>
+template <int HD, int BKV, int NQ>
 static int launch_attn_cfg(const void* qkv, void* out, const int32_t* cu, int n_seq, int max_s, int heads,
                            float scale, int64_t total_rows, cudaStream_t stream) {
-  using C = TcAttnCfg<HD, BKV, NQ, PT>;
+  using C = TcAttnCfg<HD, BKV, NQ>;
   const uint64_t ld = 3ull * heads * HD;
   const uint64_t dims[2] = {ld, static_cast<uint64_t>(total_rows)};
   const uint64_t strides[1] = {ld * 2};
@@ -425,13 +398,13 @@ static int launch_attn_cfg(const void* qkv, void* out, const int32_t* cu, int n_
   if (!C::kRem) { tqr = tq; tkvr = tkv; }
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_tc<HD, BKV, NQ, PT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_tc<HD, BKV, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmem);
     if (e != cudaSuccess) return set_cuda_error(e, "attention_tc: cudaFuncSetAttribute");
     attr = true;
   }
   dim3 grid((max_s + NQ * kTcBQ - 1) / (NQ * kTcBQ), heads, n_seq);
-  attn_fwd_tc<HD, BKV, NQ, PT><<<grid, C::kThreads, C::kSmem, stream>>>(
+  attn_fwd_tc<HD, BKV, NQ><<<grid, C::kThreads, C::kSmem, stream>>>(
       tq, tqr, tkv, tkvr, reinterpret_cast<__nv_bfloat16*>(out), cu, heads, scale * 1.4426950408889634f);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "attention_tc: launch");
@@ -444,8 +417,8 @@ static int launch_attn_cfg(const void* qkv, void* out, const int32_t* cu, int n_
 template <int HD>
 int launch_attn_tc(const void* qkv, void* out, const int32_t* cu, int n_seq, int max_s, int heads, float scale,
                    int64_t total_rows, cudaStream_t stream) {
-  if constexpr (HD == 64) return launch_attn_cfg<HD, 64, 3, true>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, stream);
-  else return launch_attn_cfg<HD, 112, 2, true>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, stream);
+  if constexpr (HD == 64) return launch_attn_cfg<HD, 64, 3>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, stream);
+  else return launch_attn_cfg<HD, 112, 2>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, stream);
 }
 
 template int launch_attn_tc<64>(const void*, void*, const int32_t*, int, int, int, float, int64_t, cudaStream_t);
