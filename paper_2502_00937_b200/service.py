@@ -193,12 +193,14 @@ class ImagePathService:
 
     def __init__(self, spec: ModelSpec, executor=None, rank: int = 0, world: int = 1,
                  policies: pol.PolicySet | None = None, max_batch: dict | None = None, cost_ms=None,
-                 ttft_slo_ms: float = 1e9):
+                 ttft_slo_ms: float = 1e9, connector=None):
         self.spec, self.executor, self.rank, self.world = spec, executor, rank, world
         self.policies = policies or pol.PolicySet()
         self.max_batch = max_batch or {StageKind.ENCODE.value: 8}
         self.cost_ms = cost_ms or (lambda tiles: 10.0 * tiles)
         self.ttft_slo_ms = ttft_slo_ms
+        self.connector = connector  # optional LLM-side projector applied on rank 0 as shards land
+        self.projected = {}
 
     def plan(self, requests):
         """Per-rank WorkItems (one ENCODE item per routed shard) + shard counts per request."""
@@ -262,6 +264,8 @@ class ImagePathService:
                     rows1 = rows0 + sum(out.image_tokens[a:b])
                     if self.rank == 0:
                         arrived_at_0[(it.request_id, it.shard_id)] = t_done
+                        if self.connector is not None:
+                            self.projected[(it.request_id, it.shard_id)] = self.connector(out.embeds[rows0:rows1])
                     else:
                         channel.send(it.request_id, it.shard_id, out.embeds[rows0:rows1])
                 inflight = None
@@ -280,8 +284,10 @@ class ImagePathService:
                     n_batches += 1
                     progressed = True
             if self.rank == 0 and channel is not None:
-                for rid, sid, _ in channel.poll():
+                for rid, sid, emb in channel.poll():
                     arrived_at_0[(rid, sid)] = clock()
+                    if self.connector is not None:
+                        self.projected[(rid, sid)] = self.connector(emb)
                     progressed = True
             mine_done = nxt == len(pending) and not queue and inflight is None
             if self.rank == 0:

@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--scheduler", default="slo_priority", choices=["fifo", "slo_priority"])
     ap.add_argument("--ms-per-tile", type=float, default=5.0, help="routing cost model (measured ~4.9 on B200)")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--connector", action="store_true", help="apply the LLM-side projector on rank 0 as shards land")
     args = ap.parse_args()
 
     import torch
@@ -63,8 +64,12 @@ def main():
     torch.cuda.synchronize()
     pol = policies.PolicySet(router=policies.RouterKind.LEAST_PENDING,
                              scheduler=policies.SchedulerKind(args.scheduler), max_fanout=8, aging_slo_fraction=0.5)
+    connector = None
+    if args.connector and rank == 0:
+        from paper_2502_00937_b200.connector import Projector
+        connector = Projector(spec)
     svc = ImagePathService(spec, ex, rank=rank, world=world, policies=pol, max_batch={"encode": args.max_batch},
-                           cost_ms=lambda tiles: args.ms_per_tile * tiles, ttft_slo_ms=2000.0)
+                           cost_ms=lambda tiles: args.ms_per_tile * tiles, ttft_slo_ms=2000.0, connector=connector)
     chan = ShardChannel(rank, world, torch.device("cuda", local), torch.bfloat16, ctrl_group=ctrl) if world > 1 else None
     res = svc.replay(reqs, channel=chan, barrier=(dist.barrier if world > 1 else None))
     if rank == 0:
@@ -75,6 +80,7 @@ def main():
                           "rate_req_s": args.rate * world, "burst": [burst.start_ms, burst.duration_ms, burst.rate_multiplier],
                           "images_per_request": IMAGES_PER_REQUEST, "requests": len(reqs), "images": n_img},
                 "batcher": {"router": "least_pending", "scheduler": args.scheduler, "max_batch_encode": args.max_batch},
+                "connector": "mllama multi_modal_projector on rank 0" if args.connector else None,
                 "model": spec.name}
         print(json.dumps(line), flush=True)
     if world > 1:

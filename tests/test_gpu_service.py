@@ -51,3 +51,37 @@ def test_executor_run_item_spans_match_direct_encode():
     torch.cuda.synchronize()
     assert out.item_spans == {0: (0, 1), 1: (1, 2)}
     assert torch.equal(out.embeds, direct.embeds)
+
+
+@pytest.mark.parametrize("model", ["llama3.2-11b", "llava-clip-l14-336"])
+def test_projector_matches_torch(model):
+    from paper_2502_00937_b200 import core
+    from paper_2502_00937_b200.connector import Projector
+    spec = core.get_model_spec(model)
+    proj = Projector(spec)
+    x = (torch.randn(3000, proj.in_dim, device="cuda") * 0.5).bfloat16()
+    got = proj(x).float()
+    ref = proj.reference(x)
+    rel = ((got - ref).norm() / ref.norm()).item()
+    assert got.shape == (3000, 4096) and rel < 1e-2, rel
+
+
+def test_replay_with_connector_projects_every_shard():
+    from paper_2502_00937_b200 import core, workload
+    from paper_2502_00937_b200.connector import Projector
+    from paper_2502_00937_b200.executor import ImagePathExecutor
+    from paper_2502_00937_b200.service import ImagePathService
+    import dataclasses
+    base = core.get_model_spec("llama3.2-11b")
+    spec = dataclasses.replace(base, encoder=dataclasses.replace(base.encoder, layers=1, global_layers=1,
+                                                                 out_layers=(1,)))
+    cfg = workload.GeneratorConfig(model=spec, base_rate=20.0, image_request_fraction=1.0,
+                                   images_per_request={1: .6, 2: .4}, seed=2)
+    reqs = workload.generate(cfg, 800.0)
+    svc = ImagePathService(spec, ImagePathExecutor(spec, seed=0), connector=Projector(spec))
+    svc.replay(reqs)
+    torch.cuda.synchronize()
+    assert len(svc.projected) == len(reqs)
+    for (rid, sid), y in svc.projected.items():
+        r = next(r for r in reqs if r.id == rid)
+        assert y.shape == (r.total_image_tokens, 4096)
