@@ -339,6 +339,31 @@ def main():
     e_value = world * B * args.steps / (float(t.item()) / 1000.0)
     assert np.isfinite(float(cks.item()))
 
+    # --------------------------------------------------------------- e2e from JPEG bytes (GPU decode)
+    e2e_jpeg = None
+    try:
+        from torchvision.io import encode_jpeg
+        jpegs = [encode_jpeg(torch.from_numpy(np.ascontiguousarray(im.transpose(2, 0, 1))), quality=90) for im in imgs]
+        o = ex.encode_jpegs(jpegs)
+        barrier()
+        j_start, j_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        jb = 0
+        j_start.record(stream)
+        for _ in range(args.steps):
+            o = ex.encode_jpegs(jpegs)
+            ops.checksum(o.embeds, out=ck)
+            offs = o.tok_offsets.to("cpu", non_blocking=True)
+            jb = sum(int(j.numel()) for j in jpegs)
+        j_end.record(stream)
+        barrier()
+        t = torch.tensor([j_start.elapsed_time(j_end)], device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_jpeg = {"value": round(world * B * args.steps / (float(t.item()) / 1000.0), 3), "unit": "images/s",
+                    "h2d_bytes_per_step": jb, "path": "ImagePathExecutor.encode_jpegs (nvJPEG decode on the GPU)"}
+    except Exception as exc:  # torchvision without CUDA JPEG support: report why
+        e2e_jpeg = {"unavailable": str(exc)[:200]}
+
     if rank == 0:
         sus, burst, hbm, src = measured_peaks()
         g = kernels.get("gemm", {"ms": 0, "work": 0, "launches": 0})
@@ -387,6 +412,7 @@ def main():
             "e2e": {"value": round(e_value, 3), "unit": "images/s", "h2d_bytes_per_step": h2d // args.steps,
                     "d2h_bytes_per_step": d2h // args.steps,
                     "path": "ImagePathExecutor.encode(stage_images(pinned host uint8)) + checksum D2H"},
+            "e2e_jpeg": e2e_jpeg,
             "clocks": clk.result(),
         }
         if not args.no_cpu_baseline and world == 1:

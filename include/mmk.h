@@ -72,7 +72,8 @@ int mmk_tile_index(const int64_t* tile_off, int32_t n, int32_t* tile_image, int3
 
 /*
  * K1 — fused uint8 HWC -> resize (bilinear, fp32) -> pad -> normalize -> tile -> patchify.
- *   src       : concatenated uint8 RGB HWC images; src_off[n] byte offsets
+ *   src       : concatenated uint8 RGB images; src_off[n] byte offsets; src_chw = 0: HWC
+ *               (interleaved, host decoders), 1: CHW planes (GPU JPEG decode output)
  *   w, h      : source dims; tile_off[n+1], geom[n*4] from mmk_tile_plan
  *   mode      : 0 = canvas fit + zero pad (Mllama), 1 = shortest-side resize + centre crop (CLIP)
  *   scale3[3], shift3[3]: normalisation out = (v * (1/255) - mean) * (1/std) as two fp32 ops:
@@ -80,11 +81,11 @@ int mmk_tile_index(const int64_t* tile_off, int32_t n, int32_t* tile_image, int3
  *   patches   : bf16 [total_tiles * (T/p)^2, k_pad], patch vector order (c, py, px) like
  *               nn.Conv2d weight flattening; columns [3*p*p, k_pad) are zero-filled.
  */
-int mmk_preprocess(const uint8_t* src, const int64_t* src_off, const int32_t* w, const int32_t* h,
-                   const int64_t* tile_off, const int32_t* geom, int32_t n, int32_t total_tiles,
-                   int32_t tile_px, int32_t patch_px, int32_t k_pad, int32_t mode,
-                   int32_t thumbnail, const float* scale3, const float* shift3, void* patches,
-                   cudaStream_t stream);
+int mmk_preprocess(const uint8_t* src, const int64_t* src_off, int32_t src_chw, const int32_t* w,
+                   const int32_t* h, const int64_t* tile_off, const int32_t* geom, int32_t n,
+                   int32_t total_tiles, int32_t tile_px, int32_t patch_px, int32_t k_pad,
+                   int32_t mode, int32_t thumbnail, const float* scale3, const float* shift3,
+                   void* patches, cudaStream_t stream);
 
 /*
  * K2/K4/K6/K7/K8 — D[M,N] = A[M,K] . B[N,K]^T on tcgen05 tensor cores (bf16 in, fp32 acc),

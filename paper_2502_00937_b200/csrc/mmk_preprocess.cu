@@ -21,6 +21,7 @@ struct PrepImage {
   int64_t off;
 };
 
+template <bool CHW>
 MMK_DEV float bilinear_u8(const uint8_t* __restrict__ img, int w, int h, int c, float sclx, float scly, int X,
                           int Y) {
   float sx = __fsub_rn(__fmul_rn(__fadd_rn(static_cast<float>(X), 0.5f), sclx), 0.5f);
@@ -33,16 +34,18 @@ MMK_DEV float bilinear_u8(const uint8_t* __restrict__ img, int w, int h, int c, 
   const int x1 = min(x0 + 1, w - 1), y1 = min(y0 + 1, h - 1);
   const float fx = __fsub_rn(sx, static_cast<float>(x0));
   const float fy = __fsub_rn(sy, static_cast<float>(y0));
-  const float p00 = img[(static_cast<int64_t>(y0) * w + x0) * 3 + c];
-  const float p01 = img[(static_cast<int64_t>(y0) * w + x1) * 3 + c];
-  const float p10 = img[(static_cast<int64_t>(y1) * w + x0) * 3 + c];
-  const float p11 = img[(static_cast<int64_t>(y1) * w + x1) * 3 + c];
+  auto px = [&](int y, int x) -> float {
+    if constexpr (CHW) return img[(static_cast<int64_t>(c) * h + y) * w + x];
+    else return img[(static_cast<int64_t>(y) * w + x) * 3 + c];
+  };
+  const float p00 = px(y0, x0), p01 = px(y0, x1), p10 = px(y1, x0), p11 = px(y1, x1);
   const float gx = __fsub_rn(1.f, fx), gy = __fsub_rn(1.f, fy);
   const float top = __fadd_rn(__fmul_rn(gx, p00), __fmul_rn(fx, p01));
   const float bot = __fadd_rn(__fmul_rn(gx, p10), __fmul_rn(fx, p11));
   return __fadd_rn(__fmul_rn(gy, top), __fmul_rn(fy, bot));
 }
 
+template <bool CHW>
 __global__ void __launch_bounds__(256)
 preprocess_kernel(const uint8_t* __restrict__ src, const int64_t* __restrict__ src_off, const int32_t* __restrict__ w,
                   const int32_t* __restrict__ h, const int64_t* __restrict__ tile_off,
@@ -115,7 +118,7 @@ preprocess_kernel(const uint8_t* __restrict__ src, const int64_t* __restrict__ s
           const int X = ox + pc * p + ix;
           const int Y = oy + pr * p + iy;
           float v = 0.f;  // padding pixel value (before normalisation), as HF Mllama pads with 0
-          if (is_thumb || crop || (X < m.nw && Y < m.nh)) v = bilinear_u8(img, m.w, m.h, c, sclx, scly, X, Y);
+          if (is_thumb || crop || (X < m.nw && Y < m.nh)) v = bilinear_u8<CHW>(img, m.w, m.h, c, sclx, scly, X, Y);
           val = __fadd_rn(__fmul_rn(v, s_scale[c]), s_shift[c]);
         }
         v2[u] = val;
@@ -130,7 +133,8 @@ preprocess_kernel(const uint8_t* __restrict__ src, const int64_t* __restrict__ s
 
 using namespace mmk;
 
-extern "C" int mmk_preprocess(const uint8_t* src, const int64_t* src_off, const int32_t* w, const int32_t* h,
+extern "C" int mmk_preprocess(const uint8_t* src, const int64_t* src_off, int32_t src_chw, const int32_t* w,
+                              const int32_t* h,
                               const int64_t* tile_off, const int32_t* geom, int32_t n, int32_t total_tiles,
                               int32_t tile_px, int32_t patch_px, int32_t k_pad, int32_t mode, int32_t thumbnail,
                               const float* scale3, const float* shift3, void* patches, cudaStream_t stream) {
@@ -141,8 +145,14 @@ extern "C" int mmk_preprocess(const uint8_t* src, const int64_t* src_off, const 
   if (reinterpret_cast<uintptr_t>(patches) & 15) return set_error(MMK_ERR_ARG, "preprocess: patches not 16B aligned");
   if (n == 0 || total_tiles == 0) return MMK_OK;
   const int blocks = total_tiles * (tile_px / patch_px);
-  preprocess_kernel<<<blocks, 256, 0, stream>>>(src, src_off, w, h, tile_off, geom, n, tile_px, patch_px, k_pad, mode,
-                                                thumbnail, scale3, shift3, reinterpret_cast<__nv_bfloat16*>(patches));
+  if (src_chw)
+    preprocess_kernel<true><<<blocks, 256, 0, stream>>>(src, src_off, w, h, tile_off, geom, n, tile_px, patch_px, k_pad,
+                                                        mode, thumbnail, scale3, shift3,
+                                                        reinterpret_cast<__nv_bfloat16*>(patches));
+  else
+    preprocess_kernel<false><<<blocks, 256, 0, stream>>>(src, src_off, w, h, tile_off, geom, n, tile_px, patch_px,
+                                                         k_pad, mode, thumbnail, scale3, shift3,
+                                                         reinterpret_cast<__nv_bfloat16*>(patches));
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "preprocess: launch");
 }

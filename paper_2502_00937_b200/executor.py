@@ -35,6 +35,7 @@ class ImageBatch:
     h: torch.Tensor            # int32 [n]
     dims: list                 # host [(w, h)]
     h2d_bytes: int = 0
+    chw: bool = False          # pixel layout of src: HWC (host decoders) or CHW planes (GPU JPEG decode)
 
     @property
     def n(self) -> int:
@@ -107,6 +108,26 @@ class CapturedEncode:
         return self.output
 
 
+def stage_jpegs(jpegs, device="cuda") -> ImageBatch:
+    """Decode JPEG byte strings on the GPU (nvJPEG via torchvision) straight into one flat device
+    buffer of CHW planes; only the compressed bytes cross PCIe."""
+    from torchvision.io import ImageReadMode, decode_jpeg
+    dev = torch.device(device)
+    datas = [j if isinstance(j, torch.Tensor) else torch.frombuffer(bytearray(j), dtype=torch.uint8) for j in jpegs]
+    imgs = decode_jpeg(datas, mode=ImageReadMode.RGB, device=dev)
+    dims = [(int(t.shape[2]), int(t.shape[1])) for t in imgs]
+    sizes = np.array([w * h * 3 for w, h in dims], np.int64)
+    offs = np.zeros(len(imgs), np.int64)
+    offs[1:] = np.cumsum(sizes)[:-1]
+    src = torch.cat([t.reshape(-1) for t in imgs]) if imgs else torch.empty(0, dtype=torch.uint8, device=dev)
+    meta = np.concatenate([offs.view(np.int32), np.array([d[0] for d in dims], np.int32),
+                           np.array([d[1] for d in dims], np.int32)])
+    dmeta = torch.from_numpy(meta).pin_memory().to(dev, non_blocking=True)
+    n = len(imgs)
+    return ImageBatch(src=src, src_off=dmeta[:2 * n].view(torch.int64), w=dmeta[2 * n:3 * n], h=dmeta[3 * n:4 * n],
+                      dims=dims, h2d_bytes=int(sum(d.numel() for d in datas)) + meta.nbytes, chw=True)
+
+
 class ImagePathExecutor:
     """preprocess -> encode -> pack for one model on one GPU (one process per GPU)."""
 
@@ -131,7 +152,7 @@ class ImagePathExecutor:
         plan = ops.tile_plan(batch.w, batch.h, spec)
         patches = ops.preprocess(batch.src, batch.src_off, batch.w, batch.h, plan["tile_off"], plan["geom"], n,
                                  total_tiles, spec, self.encoder.k_pad, self.encoder.norm_scale,
-                                 self.encoder.norm_shift)
+                                 self.encoder.norm_shift, chw=batch.chw)
         # attention sequences: all tokens of one image (images never attend to each other)
         seq_len = np.asarray(tiles, np.float64) * (P + 1)
         cu = (plan["tile_off"] * (P + 1)).to(torch.int32)  # device-side: capturable in a CUDA graph
@@ -157,6 +178,10 @@ class ImagePathExecutor:
 
     def encode_images(self, images, pinned: bool = True) -> PackedBatch:
         return self.encode(stage_images(images, self.device, pinned))
+
+    def encode_jpegs(self, jpegs) -> PackedBatch:
+        """JPEG bytes -> GPU decode -> K0..K9 (no host pixel handling at all)."""
+        return self.encode(stage_jpegs(jpegs, self.device))
 
     # ------------------------------------------------------------------ batcher API
     def run(self, batch: list[WorkItem], images: dict) -> PackedBatch:

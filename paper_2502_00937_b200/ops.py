@@ -107,14 +107,14 @@ def tile_index(tile_off: torch.Tensor, n: int, total_tiles: int):
 
 
 def preprocess(src, src_off, w, h, tile_off, geom, n: int, total_tiles: int, spec, k_pad: int,
-               scale3: torch.Tensor, shift3: torch.Tensor, out: torch.Tensor | None = None):
+               scale3: torch.Tensor, shift3: torch.Tensor, out: torch.Tensor | None = None, chw: bool = False):
     """K1: uint8 images -> bf16 patch matrix [total_tiles * P, k_pad]."""
     enc = spec.encoder
     P = (spec.tile_edge_px // enc.patch_px) ** 2
     if out is None:
         out = torch.empty(total_tiles * P, k_pad, dtype=torch.bfloat16, device=src.device)
     _t0 = _begin()
-    _lib.check(_lib.lib.mmk_preprocess(src.data_ptr(), src_off.data_ptr(), w.data_ptr(), h.data_ptr(),
+    _lib.check(_lib.lib.mmk_preprocess(src.data_ptr(), src_off.data_ptr(), int(chw), w.data_ptr(), h.data_ptr(),
                                        tile_off.data_ptr(), geom.data_ptr(), n, total_tiles, spec.tile_edge_px,
                                        enc.patch_px, k_pad, enc.resize_mode, int(spec.thumbnail_tile),
                                        scale3.data_ptr(), shift3.data_ptr(), out.data_ptr(), _s()))

@@ -240,3 +240,44 @@ def test_pack_drop_cls(mk):
     assert torch.equal(out, src.view(4, 577, 1024)[:, 1:].reshape(-1, 1024).bfloat16())
     srcb = src.bfloat16()
     assert torch.equal(ops.pack_drop_cls(srcb, 4, 577, 0), srcb)
+
+
+def test_preprocess_chw_layout_bit_identical_to_hwc(mk):
+    core, ops, encoders = mk
+    from paper_2502_00937_b200.executor import ImageBatch, stage_images
+    spec = core.get_model_spec("llama3.2-11b")
+    dims = [(700, 500), (1200, 1200), (64, 900)]
+    imgs = _rand_images(dims, 11)
+    b = stage_images(imgs)
+    chw = torch.cat([torch.from_numpy(np.ascontiguousarray(i.transpose(2, 0, 1))).reshape(-1) for i in imgs]).cuda()
+    bc = ImageBatch(src=chw, src_off=b.src_off, w=b.w, h=b.h, dims=b.dims, chw=True)
+    tiles = sum(core.tile_count(w, h, spec) for w, h in dims)
+    plan = ops.tile_plan(b.w, b.h, spec)
+    enc = spec.encoder
+    scale, shift = oprep.norm_constants(enc.mean, enc.std)
+    args = (len(dims), tiles, spec, encoders.k_pad_of(spec), torch.from_numpy(scale).cuda(), torch.from_numpy(shift).cuda())
+    a = ops.preprocess(b.src, b.src_off, b.w, b.h, plan["tile_off"], plan["geom"], *args)
+    c = ops.preprocess(bc.src, bc.src_off, bc.w, bc.h, plan["tile_off"], plan["geom"], *args, chw=True)
+    assert torch.equal(a, c)
+
+
+def test_gpu_jpeg_decode_path(mk):
+    core, ops, encoders = mk
+    pytest.importorskip("torchvision")
+    from torchvision.io import decode_jpeg, encode_jpeg
+    import dataclasses
+    from paper_2502_00937_b200.executor import ImagePathExecutor, stage_jpegs
+    base = core.get_model_spec("llama3.2-11b")
+    spec = dataclasses.replace(base, encoder=dataclasses.replace(base.encoder, layers=1, global_layers=1,
+                                                                 out_layers=(1,)))
+    imgs = _rand_images([(640, 480), (300, 900)], 4)
+    jpegs = [encode_jpeg(torch.from_numpy(np.ascontiguousarray(i.transpose(2, 0, 1))), quality=90) for i in imgs]
+    b = stage_jpegs(jpegs)
+    assert b.dims == [(640, 480), (300, 900)] and b.chw
+    ex = ImagePathExecutor(spec, seed=0)
+    out = ex.encode(b)
+    # the same decoded pixels through the HWC host path give identical embeddings
+    dec = [decode_jpeg(j, device="cuda").permute(1, 2, 0).contiguous().cpu().numpy() for j in jpegs]
+    ref = ex.encode_images(dec)
+    torch.cuda.synchronize()
+    assert torch.equal(out.embeds, ref.embeds)
