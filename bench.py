@@ -181,7 +181,7 @@ def cpu_reference_time(spec, dims, weights, threads: int):
     return time.perf_counter() - t0
 
 
-def run_reference(args, spec, wl, rank, world):
+def run_reference(args, spec, wl, rank, world, out=None):
     """--impl reference: CPU implementation of the path on this box's host cores (rank 0 only)."""
     if rank != 0:
         return
@@ -210,12 +210,22 @@ def run_reference(args, spec, wl, rank, world):
                                    f"numpy preprocess + torch fp32 encoder on {threads} threads"},
         "e2e": {"value": round(val, 4), "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=out or sys.stdout, flush=True)
 
 
 # ----------------------------------------------------------------------------- GPU path
+def _reserve_stdout_for_result():
+    """The driver parses exactly one JSON line from stdout: send everything else (NCCL's banner,
+    library prints) to stderr and keep a private handle on the real stdout for the result."""
+    sys.stdout.flush()
+    fd = os.dup(1)
+    os.dup2(2, 1)
+    return os.fdopen(fd, "w", buffering=1)
+
+
 def main():
     args = parse()
+    result_out = _reserve_stdout_for_result()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -223,7 +233,7 @@ def main():
     spec = core.get_model_spec(args.model)
     wl = WORKLOADS[args.model]
     if args.impl == "reference":
-        return run_reference(args, spec, wl, rank, world)
+        return run_reference(args, spec, wl, rank, world, out=result_out)
 
     import torch
     import torch.distributed as dist
@@ -424,7 +434,7 @@ def main():
                                     "sample": f"first {len(sample)} images of the workload "
                                               f"({sum(tiles[:len(sample)])} tiles), oracle numpy preprocess + "
                                               f"torch fp32 encoder, {dt:.1f} s"}
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=result_out, flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -95,7 +95,17 @@ class ShardChannel:
     through a queue, so sources may finish shards in any order (real-time batching).  A header
     with request id -1 ends a source's stream."""
 
-    def __init__(self, rank: int, world: int, device, dtype, ctrl_group=None, data_group=None):
+    @staticmethod
+    def make_groups(world: int, backend_data: str | None = None):
+        """Dedicated two-rank groups per source (control on gloo, data on the default backend):
+        point-to-point traffic of different sources never serialises on a shared group.  Every
+        rank must call this (group creation is collective)."""
+        import torch.distributed as dist
+        ctrl = {src: dist.new_group([0, src], backend="gloo") for src in range(1, world)}
+        data = {src: dist.new_group([0, src], backend=backend_data) for src in range(1, world)}
+        return ctrl, data
+
+    def __init__(self, rank: int, world: int, device, dtype, ctrl_group=None, data_group=None, on_arrival=None):
         import queue
         import threading
 
@@ -104,6 +114,7 @@ class ShardChannel:
         self.torch, self.dist = torch, dist
         self.rank, self.world, self.device, self.dtype = rank, world, device, dtype
         self.ctrl, self.data = ctrl_group, data_group
+        self.on_arrival = on_arrival  # runs in the receiver thread, on its private stream
         self.outgoing = []
         self.ready = queue.Queue()
         self.ended = 0
@@ -117,28 +128,34 @@ class ShardChannel:
     def _recv_loop(self, src):
         torch, dist = self.torch, self.dist
         if self.device.type == "cuda":
+            # receives are ordered on a private stream: an NCCL op waits for the *current* stream,
+            # which must not be the stream the replay loop keeps busy with encode batches
             torch.cuda.set_device(self.device)
+            torch.cuda.set_stream(torch.cuda.Stream(self.device))
         while True:
             hdr = torch.empty(4, dtype=torch.int64)
-            dist.recv(hdr, src, group=self.ctrl)
+            dist.recv(hdr, src, group=self._g(self.ctrl, src))
             rid, sid, rows, width = (int(v) for v in hdr.tolist())
             if rid < 0:
                 self.ready.put(None)
                 return
             buf = torch.empty(rows, width, dtype=self.dtype, device=self.device)
-            work = dist.irecv(buf, src, group=self.data)
+            work = dist.irecv(buf, src, group=self._g(self.data, src))
             if self.device.type == "cuda":
                 import time as _t
                 while not work.is_completed():  # NCCL: completion of the receive on the GPU
-                    _t.sleep(0.0001)
+                    _t.sleep(0.0005)  # coarse poll: keeps the GIL free for the replay loop
             else:
                 work.wait()
-            self.ready.put((rid, sid, buf))
+            extra = self.on_arrival(buf) if self.on_arrival is not None else None
+            if self.device.type == "cuda":
+                buf.record_stream(torch.cuda.default_stream(self.device))  # consumed by the replay loop
+            self.ready.put((rid, sid, buf if extra is None else extra))
 
     def send(self, req_id: int, shard_id: int, emb) -> None:
         h = self.torch.tensor([req_id, shard_id, emb.shape[0], emb.shape[1]], dtype=self.torch.int64)
-        self.dist.send(h, 0, group=self.ctrl)
-        w2 = self.dist.isend(emb.contiguous(), 0, group=self.data)
+        self.dist.send(h, 0, group=self._g(self.ctrl, self.rank))
+        w2 = self.dist.isend(emb.contiguous(), 0, group=self._g(self.data, self.rank))
         self.outgoing.append((w2, emb))
         if self.device.type == "cuda":
             self.outgoing = [o for o in self.outgoing if not o[0].is_completed()]
@@ -161,13 +178,18 @@ class ShardChannel:
         if self.rank != 0:
             for w, _ in self.outgoing:
                 w.wait()
-            self.dist.send(self.torch.tensor([-1, -1, 0, 0], dtype=self.torch.int64), 0, group=self.ctrl)
+            self.dist.send(self.torch.tensor([-1, -1, 0, 0], dtype=self.torch.int64), 0,
+                           group=self._g(self.ctrl, self.rank))
         else:
             for th in self.threads:
                 th.join(timeout=60)
 
     def finished_sources(self) -> int:
         return self.ended
+
+    @staticmethod
+    def _g(group, src):
+        return group.get(src) if isinstance(group, dict) else group
 
 
 @dataclass
@@ -200,7 +222,7 @@ class ImagePathService:
         self.cost_ms = cost_ms or (lambda tiles: 10.0 * tiles)
         self.ttft_slo_ms = ttft_slo_ms
         self.connector = connector  # optional LLM-side projector applied on rank 0 as shards land
-        self.projected = {}
+        self.projected = {}         # (request id, shard id) -> projected shape (outputs go to prefill, not kept)
 
     def plan(self, requests):
         """Per-rank WorkItems (one ENCODE item per routed shard) + shard counts per request."""
@@ -265,7 +287,8 @@ class ImagePathService:
                     if self.rank == 0:
                         arrived_at_0[(it.request_id, it.shard_id)] = t_done
                         if self.connector is not None:
-                            self.projected[(it.request_id, it.shard_id)] = self.connector(out.embeds[rows0:rows1])
+                            y = self.connector(out.embeds[rows0:rows1])
+                            self.projected[(it.request_id, it.shard_id)] = tuple(y.shape)
                     else:
                         channel.send(it.request_id, it.shard_id, out.embeds[rows0:rows1])
                 inflight = None
@@ -284,10 +307,10 @@ class ImagePathService:
                     n_batches += 1
                     progressed = True
             if self.rank == 0 and channel is not None:
-                for rid, sid, emb in channel.poll():
+                for rid, sid, item in channel.poll():
                     arrived_at_0[(rid, sid)] = clock()
                     if self.connector is not None:
-                        self.projected[(rid, sid)] = self.connector(emb)
+                        self.projected[(rid, sid)] = tuple(item.shape)
                     progressed = True
             mine_done = nxt == len(pending) and not queue and inflight is None
             if self.rank == 0:

@@ -34,7 +34,11 @@ def main():
     ap.add_argument("--ms-per-tile", type=float, default=5.0, help="routing cost model (measured ~4.9 on B200)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--connector", action="store_true", help="apply the LLM-side projector on rank 0 as shards land")
+    ap.add_argument("--watchdog-s", type=float, default=0.0, help="dump all thread stacks after this many seconds")
     args = ap.parse_args()
+    if args.watchdog_s > 0:
+        import faulthandler
+        faulthandler.dump_traceback_later(args.watchdog_s, exit=True)
 
     import torch
     import torch.distributed as dist
@@ -46,10 +50,14 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    ctrl = None
+    result_out = sys.stdout
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        ctrl = dist.new_group(backend="gloo")
+        sys.stdout.flush()
+        result_out = os.fdopen(os.dup(1), "w", buffering=1)  # NCCL banners -> stderr
+        os.dup2(2, 1)
+        # lazy NCCL communicator init: the per-source two-rank groups are created collectively
+        # below and each connects on its first transfer
+        dist.init_process_group("nccl")
     spec = core.get_model_spec(args.model)
     horizon = args.duration_s * 1000.0
     burst = workload.BurstEpisode(start_ms=0.4 * horizon, duration_ms=0.2 * horizon, rate_multiplier=args.burst_mult)
@@ -70,7 +78,12 @@ def main():
         connector = Projector(spec)
     svc = ImagePathService(spec, ex, rank=rank, world=world, policies=pol, max_batch={"encode": args.max_batch},
                            cost_ms=lambda tiles: args.ms_per_tile * tiles, ttft_slo_ms=2000.0, connector=connector)
-    chan = ShardChannel(rank, world, torch.device("cuda", local), torch.bfloat16, ctrl_group=ctrl) if world > 1 else None
+    chan = None
+    if world > 1:
+        ctrl_g, data_g = ShardChannel.make_groups(world)
+        # remote shards are projected by the receiver threads, on their own streams, as they land
+        chan = ShardChannel(rank, world, torch.device("cuda", local), torch.bfloat16, ctrl_group=ctrl_g,
+                            data_group=data_g, on_arrival=connector)
     res = svc.replay(reqs, channel=chan, barrier=(dist.barrier if world > 1 else None))
     if rank == 0:
         s = res.summary()
@@ -82,7 +95,7 @@ def main():
                 "batcher": {"router": "least_pending", "scheduler": args.scheduler, "max_batch_encode": args.max_batch},
                 "connector": "mllama multi_modal_projector on rank 0" if args.connector else None,
                 "model": spec.name}
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=result_out, flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
