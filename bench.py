@@ -414,9 +414,10 @@ def main():
                               "frac": round(enc_tf / sus, 4),
                               "note": "algorithmic encoder FLOPs of the whole step / step time"},
             "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
-                            "achieved": round(v["work"] / (v["ms"] / 1e3) / (1e12 if k in ("gemm", "attention") else 1e9), 1)
+                            "achieved": round(v["work"] / (v["ms"] / 1e3) /
+                                              (1e12 if (k in ("gemm", "attention") or k.startswith("gemm.")) else 1e9), 1)
                             if v["ms"] else None,
-                            "unit": "TFLOP/s" if k in ("gemm", "attention") else "GB/s"}
+                            "unit": "TFLOP/s" if (k in ("gemm", "attention") or k.startswith("gemm.")) else "GB/s"}
                         for k, v in kernels.items()},
             "gpu_launches": launches,
             "e2e": {"value": round(e_value, 3), "unit": "images/s", "h2d_bytes_per_step": h2d // args.steps,

@@ -246,15 +246,17 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
 // `tfull` are multicast by the leader's tcgen05.commit to both CTAs, `tempty` lives in the leader
 // and counts the epilogue warps of both CTAs.
 constexpr int kGemm2BN = 256;
-template <int STAGES>
+template <int STAGES, bool RESID>
 struct Gemm2Smem {
   static constexpr int kABytes = 128 * kGemmBK * 2;             // this CTA's 128 rows of A
   static constexpr int kBBytes = (kGemm2BN / 2) * kGemmBK * 2;  // this CTA's half of B
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kEpiOffset = STAGES * kStageBytes;       // 8 warps x 2 x [32 rows][128 B]
-  static constexpr int kEpiBytes = 8 * 2 * 4096;
+  static constexpr int kEpiOffset = STAGES * kStageBytes;
+  // bf16 epilogues: 8 warps x 2 x [32 rows][128 B] staging; residual epilogue: 8 warps x the
+  // warp's whole fp32 residual slice (4 chunks of [32 rows][32 fp32])
+  static constexpr int kEpiBytes = RESID ? 8 * 4 * 4096 : 8 * 2 * 4096;
   static constexpr int kBarOffset = kEpiOffset + kEpiBytes;
-  static constexpr int kTotal = kBarOffset + 256 + 1024;
+  static constexpr int kTotal = kBarOffset + 512 + 1024;
 };
 
 // bf16 epilogue through shared memory + TMA store: 32 rows x 64 cols per warp per step, staged in
@@ -294,12 +296,12 @@ MMK_DEV void epilogue_bf16_tma(const uint32_t (&r0)[32], const uint32_t (&r1)[32
   }
 }
 
-template <int STAGES, int EPI>
+template <int STAGES, int EPI, bool RES_TMA = false>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                       const __grid_constant__ CUtensorMap tmap_out, int M, int N, int K, const float* __restrict__ bias, void* __restrict__ out, int64_t ldo,
                       float gate, __nv_bfloat16* __restrict__ aux, int64_t ld_aux) {
-  using S = Gemm2Smem<STAGES>;
+  using S = Gemm2Smem<STAGES, RES_TMA>;
   constexpr int BN = kGemm2BN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -307,7 +309,8 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* tfull_bar = empty_bar + STAGES;  // [2]
   uint64_t* tempty_bar = tfull_bar + 2;      // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* res_bar = tempty_bar + 2;        // [8 warps][4 chunks] residual TMA loads (RESID)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_bar + 32);
 
   const uint32_t warp = warp_id_uniform();
   const uint32_t lane = lane_id();
@@ -328,6 +331,10 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
       mbar_init(&tempty_bar[b], 16);  // 8 epilogue warps x 2 CTAs
+    }
+    if (RES_TMA) {
+      tma_prefetch_desc(&tmap_out);
+      for (int i = 0; i < 32; ++i) mbar_init(&res_bar[i], 1);
     }
     fence_barrier_init();
   }
@@ -410,6 +417,19 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
       const uint32_t acc_phase = (t >> 1) & 1;
       const int m0 = (tile / n_tiles_n) * 256 + rank * 128;
       const int n0 = (tile % n_tiles_n) * BN;
+      if constexpr (RES_TMA) {
+        if (lane == 0) {
+          tma_store_wait_read<0>();  // the previous tile's stores have left this warp's slab
+          uint8_t* slab = smem + S::kEpiOffset + (warp - 4) * 4 * 4096;
+#pragma unroll
+          for (int c = 0; c < kColsPerWarp / 32; ++c) {
+            mbar_arrive_expect_tx(&res_bar[(warp - 4) * 4 + c], 4096);
+            tma_load_2d(&tmap_out, &res_bar[(warp - 4) * 4 + c], slab + c * 4096,
+                        n0 + half * kColsPerWarp + c * 32, m0 + static_cast<int>(q) * 32);
+          }
+        }
+        __syncwarp();
+      }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t tm_row = tmem_base + ((q * 32u) << 16) + acc * BN;
@@ -430,6 +450,64 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
                                  ebuf + sb * 4096, &tmap_out);
           sb ^= 1;
         }
+      } else if constexpr (RES_TMA) {
+        // fp32 residual read-modify-write through shared memory: the warp's whole residual slice
+        // (32 rows x 128 cols) is TMA-loaded while the tile's MMAs run (issued above), updated in
+        // place (128B-swizzled rows, conflict-free 16-byte accesses) and TMA-stored back.
+        const int row = m0 + q * 32 + lane;
+        const bool row_ok = row < M;
+        uint8_t* slab = smem + S::kEpiOffset + (warp - 4) * 4 * 4096;
+#pragma unroll 1
+        for (int c = 0; c < kColsPerWarp / 32; ++c) {
+          const int col_in_tile = half * kColsPerWarp + c * 32;
+          const int col = n0 + col_in_tile;
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tm_row + col_in_tile, r);
+          tmem_ld_wait();
+          if (c == kColsPerWarp / 32 - 1) {  // accumulator fully read: release it early
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
+          }
+          mbar_wait(&res_bar[(warp - 4) * 4 + c], t & 1);
+          uint8_t* rowp = slab + c * 4096 + lane * 128;
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+          if (bias != nullptr) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + col + i));
+              v[i] += b4.x; v[i + 1] += b4.y; v[i + 2] += b4.z; v[i + 3] += b4.w;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {  // 16-byte chunk j = columns 4j..4j+3 of this row
+            float4* p4 = reinterpret_cast<float4*>(rowp + ((j ^ (lane & 7)) << 4));
+            float4 rr = *p4;
+            rr.x = fmaf(gate, v[4 * j], rr.x);
+            rr.y = fmaf(gate, v[4 * j + 1], rr.y);
+            rr.z = fmaf(gate, v[4 * j + 2], rr.z);
+            rr.w = fmaf(gate, v[4 * j + 3], rr.w);
+            *p4 = rr;
+            v[4 * j] = rr.x; v[4 * j + 1] = rr.y; v[4 * j + 2] = rr.z; v[4 * j + 3] = rr.w;
+          }
+          if (aux != nullptr && row_ok) {
+            __nv_bfloat16* ao = aux + static_cast<int64_t>(row) * ld_aux + col;
+#pragma unroll
+            for (int i = 0; i < 32; i += 8)
+              st_global_v4(ao + i, pack_bf16x2(v[i], v[i + 1]), pack_bf16x2(v[i + 2], v[i + 3]),
+                           pack_bf16x2(v[i + 4], v[i + 5]), pack_bf16x2(v[i + 6], v[i + 7]));
+          }
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll
+          for (int c = 0; c < kColsPerWarp / 32; ++c)
+            tma_store_2d(&tmap_out, slab + c * 4096, n0 + half * kColsPerWarp + c * 32, m0 + static_cast<int>(q) * 32);
+          tma_store_commit();
+        }
       } else {
         const int row = m0 + q * 32 + lane;
         const bool row_ok = row < M;
@@ -448,7 +526,7 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
         if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
       }
     }
-    if constexpr (kTmaStore) {
+    if constexpr (kTmaStore || RES_TMA) {
       if (lane == 0) tma_store_wait<0>();
       __syncwarp();
     }
@@ -496,13 +574,13 @@ static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, i
 }
 
 
-template <int STAGES, int EPI>
+template <int STAGES, int EPI, bool RES_TMA = false>
 static int launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, int M, int N, int K,
                            const float* bias,
                            void* out, int64_t ldo, float gate, __nv_bfloat16* aux, int64_t ld_aux,
                            cudaStream_t stream) {
-  using S = Gemm2Smem<STAGES>;
-  auto kern = gemm_bf16_tcgen05_2sm<STAGES, EPI>;
+  using S = Gemm2Smem<STAGES, RES_TMA>;
+  auto kern = gemm_bf16_tcgen05_2sm<STAGES, EPI, RES_TMA>;
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
@@ -538,7 +616,11 @@ static int dispatch_epi_2sm(int epi, const CUtensorMap& ta, const CUtensorMap& t
     case MMK_EPI_BF16_GELU: return launch_gemm_2sm<STAGES, MMK_EPI_BF16_GELU>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
     case MMK_EPI_BF16_QUICKGELU: return launch_gemm_2sm<STAGES, MMK_EPI_BF16_QUICKGELU>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
     case MMK_EPI_F32: return launch_gemm_2sm<STAGES, MMK_EPI_F32>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
-    case MMK_EPI_RESID_F32: return launch_gemm_2sm<STAGES, MMK_EPI_RESID_F32>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
+    case MMK_EPI_RESID_F32:
+      // short K: the residual slice is TMA-prefetched into smem during the mainloop (3 stages);
+      // long K: the mainloop hides the direct read-modify-write, keep 5 stages
+      if (K <= 2048) return launch_gemm_2sm<3, MMK_EPI_RESID_F32, true>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
+      return launch_gemm_2sm<STAGES, MMK_EPI_RESID_F32>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
     default: return set_error(MMK_ERR_ARG, "gemm: unknown epilogue %d", epi);
   }
 }
@@ -570,9 +652,15 @@ extern "C" int mmk_gemm_bf16(const void* a, int64_t lda, const void* b, int64_t 
     if (rc) return rc;
     rc = make_tmap_2d_bf16(&tb, b, k, n, ldb, kGemmBK, 128, true);
     if (rc) return rc;
-    CUtensorMap to = tb;  // output map: bf16 epilogues only ([32 rows][64 cols], 128B swizzle)
+    CUtensorMap to = tb;  // output map: bf16 [32 rows][64 cols] or fp32 residual [32 rows][32 cols], 128B swizzle
     if (!f32_out) {
       rc = make_tmap_2d_bf16(&to, out, n, m, ldo, 64, 32, true);
+      if (rc) return rc;
+    } else if (epilogue == MMK_EPI_RESID_F32) {
+      const uint64_t dims[2] = {static_cast<uint64_t>(n), static_cast<uint64_t>(m)};
+      const uint64_t strides[1] = {static_cast<uint64_t>(ldo) * 4};
+      const uint32_t box[2] = {32, 32};
+      rc = make_tmap(&to, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, out, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
       if (rc) return rc;
     }
     return dispatch_epi_2sm<5>(epilogue, ta, tb, to, m, n, k, bias, out, ldo, gate,

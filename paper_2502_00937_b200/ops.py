@@ -11,6 +11,8 @@ from .core import SpecError
 
 EPI_BF16, EPI_BF16_GELU, EPI_BF16_QUICKGELU, EPI_F32, EPI_RESID_F32 = range(5)
 ACT_EPI = {"gelu": EPI_BF16_GELU, "quick_gelu": EPI_BF16_QUICKGELU}
+EPI_NAMES = {EPI_BF16: "bf16", EPI_BF16_GELU: "gelu", EPI_BF16_QUICKGELU: "quickgelu", EPI_F32: "f32",
+             EPI_RESID_F32: "resid"}
 
 
 class LaunchLog:
@@ -37,13 +39,16 @@ class LaunchLog:
             self.records.append((kind, work, start, e))
 
     def summary(self):
-        """kind -> dict(launches, ms_total, work_total) (call after synchronize)."""
+        """kind -> dict(launches, ms_total, work_total) (call after synchronize).  GEMM launches
+        are reported per epilogue ("gemm.resid", ...) and aggregated under "gemm"."""
         out = {}
         for kind, work, s, e in self.records:
-            d = out.setdefault(kind, {"launches": 0, "ms": 0.0, "work": 0.0})
-            d["launches"] += 1
-            d["ms"] += s.elapsed_time(e)
-            d["work"] += work
+            ms = s.elapsed_time(e)
+            for k in ((kind, "gemm") if kind.startswith("gemm.") else (kind,)):
+                d = out.setdefault(k, {"launches": 0, "ms": 0.0, "work": 0.0})
+                d["launches"] += 1
+                d["ms"] += ms
+                d["work"] += work
         return out
 
 
@@ -138,7 +143,7 @@ def gemm(a: torch.Tensor, b: torch.Tensor, epilogue: int = EPI_BF16, bias=None, 
     _lib.check(_lib.lib.mmk_gemm_bf16(a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), m, n, k, epilogue,
                                       _p(bias), out.data_ptr(), out.stride(0), float(gate), _p(aux),
                                       aux.stride(0) if aux is not None else 0, _s()))
-    _end('gemm', 2.0 * m * n * k, _t0)
+    _end(f'gemm.{EPI_NAMES[epilogue]}', 2.0 * m * n * k, _t0)
     return out
 
 
