@@ -293,6 +293,9 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
           mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2;
         }
         float m_new = m_used, corr = 1.f;
+#ifdef MMK_ATTN_XP_NOMAX  // timing experiment only (make xp): running max from the first tile
+        if (j > 0) mx = m_used;
+#endif
         if (mx > m_used + kRescaleThreshold) {
           m_new = mx;
           corr = fast_exp2(m_used - m_new);  // 0 on the first tile
@@ -322,6 +325,11 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
         for (int i = 0; i < BKV / 2; ++i) {
           const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), sc2, nm2);
           float2 e;
+#ifdef MMK_ATTN_XP_NOEXP  // timing experiment only (make xp): no exponential
+          if (true) {
+            e = x;
+          } else
+#endif
           if ((i & 7) < MMK_POLY8) {
             e = exp2_poly2(x);
           } else {

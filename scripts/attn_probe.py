@@ -9,6 +9,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2502_00937_b200 import ops  # noqa: E402
 
 
+# tiles per image of bench.py's 32-image Mllama step (reference generator, seed 0)
+BENCH_MIX = [1, 1, 1, 1, 1, 4, 2, 1, 2, 1, 4, 2, 2, 3, 4, 4, 2, 4, 4, 1, 2, 4, 2, 2, 4, 3, 1, 2, 4, 1, 1, 4]
+
+
 def ref(qkv, lens, heads, hd):
     outs, start, d = [], 0, heads * hd
     for L in lens:
@@ -44,10 +48,15 @@ def run(lens, heads, hd, iters=10, check=True):
 
 
 if __name__ == "__main__":
-    print("impl:", "legacy mma.sync" if os.environ.get("MMK_ATTN_LEGACY") else "tcgen05")
+    print("impl:", "legacy mma.sync" if os.environ.get("MMK_ATTN_LEGACY") else "tcgen05", os.environ.get("MMK_LIB", ""))
+    if os.environ.get("ATTN_PROBE_QUICK"):
+        run([t * 1601 for t in BENCH_MIX], 16, 80, check=False)
+        run([6404] * 8, 16, 80, check=False)
+        sys.exit(0)
     run([1601, 3202, 1, 63, 64, 65, 6404, 129, 255, 256, 257], 16, 80)
     run([577, 577, 129, 1], 16, 64)
     run([6404] * 8, 16, 80, check=False)
     run([1601] * 32, 16, 80, check=False)
+    run([t * 1601 for t in BENCH_MIX], 16, 80, check=False)
     run([577] * 256, 16, 64, check=False)
     run([197] * 64, 12, 64, check=False)
