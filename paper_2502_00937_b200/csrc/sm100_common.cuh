@@ -238,6 +238,57 @@ MMK_DEV void tmem_st_32x32b_x8(uint32_t taddr, const uint32_t (&r)[8]) {
                "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
                : "memory");
 }
+MMK_DEV void tmem_ld_32x32b_x8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+MMK_DEV void tmem_ld_32x32b_x4(uint32_t taddr, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
+MMK_DEV void tmem_st_32x32b_x4(uint32_t taddr, const uint32_t (&r)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(r[0]), "r"(r[1]),
+               "r"(r[2]), "r"(r[3])
+               : "memory");
+}
+// N consecutive 32-bit TMEM columns of this thread's lane (N a multiple of 4), in x32/x16/x8/x4 pieces
+template <int N>
+MMK_DEV void tmem_ld_cols(uint32_t taddr, uint32_t* r) {
+  if constexpr (N >= 32) {
+    tmem_ld_32x32b_x32(taddr, *reinterpret_cast<uint32_t(*)[32]>(r));
+    tmem_ld_cols<N - 32>(taddr + 32, r + 32);
+  } else if constexpr (N >= 16) {
+    tmem_ld_32x32b_x16(taddr, *reinterpret_cast<uint32_t(*)[16]>(r));
+    tmem_ld_cols<N - 16>(taddr + 16, r + 16);
+  } else if constexpr (N >= 8) {
+    tmem_ld_32x32b_x8(taddr, *reinterpret_cast<uint32_t(*)[8]>(r));
+    tmem_ld_cols<N - 8>(taddr + 8, r + 8);
+  } else if constexpr (N >= 4) {
+    tmem_ld_32x32b_x4(taddr, *reinterpret_cast<uint32_t(*)[4]>(r));
+    tmem_ld_cols<N - 4>(taddr + 4, r + 4);
+  }
+}
+template <int N>
+MMK_DEV void tmem_st_cols(uint32_t taddr, const uint32_t* r) {
+  if constexpr (N >= 32) {
+    tmem_st_32x32b_x32(taddr, *reinterpret_cast<const uint32_t(*)[32]>(r));
+    tmem_st_cols<N - 32>(taddr + 32, r + 32);
+  } else if constexpr (N >= 16) {
+    tmem_st_32x32b_x16(taddr, *reinterpret_cast<const uint32_t(*)[16]>(r));
+    tmem_st_cols<N - 16>(taddr + 16, r + 16);
+  } else if constexpr (N >= 8) {
+    tmem_st_32x32b_x8(taddr, *reinterpret_cast<const uint32_t(*)[8]>(r));
+    tmem_st_cols<N - 8>(taddr + 8, r + 8);
+  } else if constexpr (N >= 4) {
+    tmem_st_32x32b_x4(taddr, *reinterpret_cast<const uint32_t(*)[4]>(r));
+    tmem_st_cols<N - 4>(taddr + 4, r + 4);
+  }
+}
+MMK_DEV void named_bar_sync(uint32_t id, uint32_t threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 MMK_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 MMK_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
