@@ -372,6 +372,9 @@ def main():
         e2e_jpeg = {"value": round(world * B * args.steps / (float(t.item()) / 1000.0), 3), "unit": "images/s",
                     "h2d_bytes_per_step": jb, "path": "ImagePathExecutor.encode_jpegs (nvJPEG decode on the GPU)"}
     except Exception as exc:  # torchvision without CUDA JPEG support: report why
+        if os.environ.get("BENCH_DEBUG"):
+            import traceback
+            traceback.print_exc()
         e2e_jpeg = {"unavailable": str(exc)[:200]}
 
     if rank == 0:

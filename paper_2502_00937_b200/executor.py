@@ -108,13 +108,37 @@ class CapturedEncode:
         return self.output
 
 
+JPEG_DECODE_CHUNK = 32
+_DECODE_STREAMS: dict = {}
+
+
+def _decode_stream(dev: torch.device) -> torch.cuda.Stream:
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    if idx not in _DECODE_STREAMS:
+        _DECODE_STREAMS[idx] = torch.cuda.Stream(device=idx)
+    return _DECODE_STREAMS[idx]
+
+
 def stage_jpegs(jpegs, device="cuda") -> ImageBatch:
     """Decode JPEG byte strings on the GPU (nvJPEG via torchvision) straight into one flat device
     buffer of CHW planes; only the compressed bytes cross PCIe."""
     from torchvision.io import ImageReadMode, decode_jpeg
     dev = torch.device(device)
     datas = [j if isinstance(j, torch.Tensor) else torch.frombuffer(bytearray(j), dtype=torch.uint8) for j in jpegs]
-    imgs = decode_jpeg(datas, mode=ImageReadMode.RGB, device=dev)
+    # The decoder runs on its own stream with its own allocator pool: decoding on the compute
+    # stream let torchvision's decoder write blocks that the caching allocator had just recycled
+    # from tensors still read by in-flight kernels of the previous batch (CUDA error 700 in the
+    # back-to-back e2e loop).  The decoded planes are handed to the compute stream by event and
+    # record_stream.
+    compute = torch.cuda.current_stream(dev)
+    dec = _decode_stream(dev)
+    imgs = []
+    with torch.cuda.stream(dec):
+        for i in range(0, len(datas), JPEG_DECODE_CHUNK):
+            imgs += decode_jpeg(datas[i:i + JPEG_DECODE_CHUNK], mode=ImageReadMode.RGB, device=dev)
+    compute.wait_stream(dec)
+    for t in imgs:
+        t.record_stream(compute)
     dims = [(int(t.shape[2]), int(t.shape[1])) for t in imgs]
     sizes = np.array([w * h * 3 for w, h in dims], np.int64)
     offs = np.zeros(len(imgs), np.int64)

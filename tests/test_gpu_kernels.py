@@ -281,3 +281,22 @@ def test_gpu_jpeg_decode_path(mk):
     ref = ex.encode_images(dec)
     torch.cuda.synchronize()
     assert torch.equal(out.embeds, ref.embeds)
+
+
+def test_gpu_jpeg_decode_large_batch_chunked(mk):
+    """A few hundred JPEGs in one stage_jpegs call (decoded in chunks) keep order and pixels."""
+    core, ops, encoders = mk
+    pytest.importorskip("torchvision")
+    from torchvision.io import decode_jpeg, encode_jpeg
+    from paper_2502_00937_b200.executor import stage_jpegs
+    dims = [(64 + 7 * i, 48 + 5 * (i % 13)) for i in range(300)]
+    imgs = _rand_images(dims, 5)
+    jpegs = [encode_jpeg(torch.from_numpy(np.ascontiguousarray(i.transpose(2, 0, 1))), quality=90) for i in imgs]
+    b = stage_jpegs(jpegs)
+    torch.cuda.synchronize()
+    assert b.dims == dims
+    offs = b.src_off.cpu().numpy()
+    for i in (0, 31, 32, 150, 299):
+        ref = decode_jpeg(jpegs[i], device="cuda").reshape(-1)
+        w, h = dims[i]
+        assert torch.equal(b.src[offs[i]:offs[i] + w * h * 3], ref)
