@@ -108,6 +108,22 @@ def test_encode_shard():  # reference test_engine.py:174-191
     assert max(loads) - min(loads) <= 2
     assert batcher.encode_shard(imgs[:1], 4) == [[0]]
     assert batcher.encode_shard([], 4) == []
+    four = [core.ImageSpec.from_dims(896, 896, INTERNVL)] * 4
+    assert sorted(len(s) for s in batcher.encode_shard(four, 4)) == [1, 1, 1, 1]  # even split
+
+
+def test_sixteen_images_over_four_shards_quarter_makespan():
+    """reference test_acceptance.py:527-545 / test_engine.py:193-202: 16 equal images over 4
+    instances -> partition [4, 4, 4, 4] and an encode makespan (tiles of the largest shard) of
+    exactly 1/4 of the unsharded one, under both the reference rule and the FLOP-weighted rule."""
+    llama = core.get_model_spec("llama3.2-11b")
+    imgs = [core.ImageSpec.from_dims(896, 896, llama)] * 16
+    shards = batcher.encode_shard(imgs, 4)
+    assert [len(s) for s in shards] == [4, 4, 4, 4]
+    span = max(sum(imgs[i].tiles for i in s) for s in shards)
+    assert span * 4 == sum(im.tiles for im in imgs)
+    by_cost = policies.split_by_cost([float(im.tiles ** 2) for im in imgs], 4)
+    assert sorted(len(s) for s in by_cost) == [4, 4, 4, 4]
 
 
 def _item(seq, stage, size=10, enqueue=0.0, deps=()):
