@@ -404,13 +404,10 @@ static int launch_attn_cfg(const void* qkv, void* out, const int32_t* cu, int n_
   if (!rc && C::kRem) rc = make_tmap_bf16(&tkvr, qkv, 2, dims, strides, bkvr, CU_TENSOR_MAP_SWIZZLE_32B);
   if (rc) return rc;
   if (!C::kRem) { tqr = tq; tkvr = tkv; }
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_tc<HD, BKV, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::kSmem);
-    if (e != cudaSuccess) return set_cuda_error(e, "attention_tc: cudaFuncSetAttribute");
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  rc = ensure_smem_attr(reinterpret_cast<const void*>(attn_fwd_tc<HD, BKV, NQ>), C::kSmem, attr_done,
+                        "attention_tc: cudaFuncSetAttribute");
+  if (rc) return rc;
   dim3 grid((max_s + NQ * kTcBQ - 1) / (NQ * kTcBQ), heads, n_seq);
   attn_fwd_tc<HD, BKV, NQ><<<grid, C::kThreads, C::kSmem, stream>>>(
       tq, tqr, tkv, tkvr, reinterpret_cast<__nv_bfloat16*>(out), cu, heads, scale * 1.4426950408889634f);

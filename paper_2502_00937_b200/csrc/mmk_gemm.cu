@@ -561,12 +561,9 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int 
                        int64_t ld_aux, cudaStream_t stream) {
   using S = GemmSmem<BN, STAGES>;
   auto kern = gemm_bf16_tcgen05<BN, STAGES, EPI>;
-  static bool attr_done = false;  // per template instance
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
-    if (e != cudaSuccess) return set_cuda_error(e, "gemm: cudaFuncSetAttribute");
-    attr_done = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};  // per template instance
+  if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), S::kTotal, attr_done, "gemm: cudaFuncSetAttribute"))
+    return rc;
   const int tiles = ((M + kGemmBM - 1) / kGemmBM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   kern<<<grid, kGemmThreads, S::kTotal, stream>>>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux);
@@ -597,12 +594,9 @@ static int launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, const C
                            cudaStream_t stream) {
   using S = Gemm2Smem<STAGES>;
   auto kern = gemm_bf16_tcgen05_2sm<STAGES, EPI, RES_TMA>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kTotal);
-    if (e != cudaSuccess) return set_cuda_error(e, "gemm2: cudaFuncSetAttribute");
-    attr_done = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};  // per template instance
+  if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), S::kTotal, attr_done, "gemm2: cudaFuncSetAttribute"))
+    return rc;
   const int tiles = ((M + 255) / 256) * (N / kGemm2BN);
   const int pairs_max = num_sms() / 2;
   const int pairs = tiles < pairs_max ? tiles : pairs_max;

@@ -1,5 +1,6 @@
 // mmk_internal.h — shared host-side helpers of libmmk (error state, SM count, TMA maps).
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -20,5 +21,19 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t*
                    const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swz);
 int make_tmap(CUtensorMap* map, CUtensorMapDataType dtype, const void* base, int rank, const uint64_t* dims,
               const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swz);
+
+// Raise a kernel's dynamic shared-memory limit once per device.  `done` is a per-kernel bit set
+// of devices (a static at the call site); concurrent first calls may both set the attribute,
+// which is idempotent.
+inline int ensure_smem_attr(const void* kern, int bytes, std::atomic<uint64_t>& done, const char* what) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return MMK_OK;
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return set_cuda_error(e, what);
+  done.fetch_or(bit, std::memory_order_release);
+  return MMK_OK;
+}
 
 }  // namespace mmk
