@@ -80,3 +80,9 @@ def test_vit_b16_batch8():
     from paper_2502_00937_b200 import core
     spec = core.get_model_spec("vit-b16-224")
     _run(spec, [(224, 224)] * 8, seed=2)
+
+
+def test_clip_l336_full_depth():
+    """Full 24-layer CLIP ViT-L/14-336 to layer -2 (LLaVA feature layer), CLS dropped."""
+    from paper_2502_00937_b200 import core
+    _run(core.get_model_spec("llava-clip-l14-336"), [(336, 336), (800, 600)], seed=3)
