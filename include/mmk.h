@@ -114,10 +114,13 @@ int mmk_layernorm(const float* x, void* y, int32_t y_f32, int32_t rows, int32_t 
  *   qkv bf16 [T, 3*H*hd] = [Q | K | V] (head h at column h*hd inside each block)
  *   out bf16 [T, H*hd]; cu_seqlens int32 [n_seq+1] (device); total_tokens = T = cu_seqlens[n_seq]
  *   (host copy, bounds the TMA tensor maps); hd in {64, 80}; scale = hd^-0.5 typically.
+ *   workspace: device memory of mmk_attention_workspace_size() bytes, overwritten (the persistent
+ *   kernel's work-item counter, reset on `stream`); not to be shared by concurrent calls.
  */
+int64_t mmk_attention_workspace_size(void);
 int mmk_attention_varlen_bf16(const void* qkv, void* out, const int32_t* cu_seqlens, int32_t n_seq,
                               int32_t max_seqlen, int32_t total_tokens, int32_t heads,
-                              int32_t head_dim, float scale, cudaStream_t stream);
+                              int32_t head_dim, float scale, void* workspace, cudaStream_t stream);
 
 /*
  * Embedding assembly (feeds K3 of layer 0): patch-embed output + class token + positional

@@ -12,21 +12,23 @@
 namespace mmk {
 template <int HD>
 int launch_attn_tc(const void* qkv, void* out, const int32_t* cu, int n_seq, int max_s, int heads, float scale,
-                   int64_t total_rows, cudaStream_t stream);
+                   int64_t total_rows, void* workspace, cudaStream_t stream);
 }
 
 using namespace mmk;
 
+extern "C" int64_t mmk_attention_workspace_size(void) { return 16; }
+
 extern "C" int mmk_attention_varlen_bf16(const void* qkv, void* out, const int32_t* cu_seqlens, int32_t n_seq,
                                          int32_t max_seqlen, int32_t total_tokens, int32_t heads, int32_t head_dim,
-                                         float scale, cudaStream_t stream) {
+                                         float scale, void* workspace, cudaStream_t stream) {
   if (n_seq < 0 || heads <= 0 || max_seqlen < 0 || total_tokens < 0)
     return set_error(MMK_ERR_ARG, "attention: bad shape");
   if (head_dim != 64 && head_dim != 80)
     return set_error(MMK_ERR_UNSUPPORTED, "attention: head_dim %d not in {64, 80}", head_dim);
   if (n_seq == 0 || max_seqlen == 0 || total_tokens == 0) return MMK_OK;
-  if (n_seq > 65535 || heads > 65535) return set_error(MMK_ERR_UNSUPPORTED, "attention: too many sequences/heads");
+  if (workspace == nullptr) return set_error(MMK_ERR_ARG, "attention: workspace is NULL");
   if (head_dim == 64)
-    return launch_attn_tc<64>(qkv, out, cu_seqlens, n_seq, max_seqlen, heads, scale, total_tokens, stream);
-  return launch_attn_tc<80>(qkv, out, cu_seqlens, n_seq, max_seqlen, heads, scale, total_tokens, stream);
+    return launch_attn_tc<64>(qkv, out, cu_seqlens, n_seq, max_seqlen, heads, scale, total_tokens, workspace, stream);
+  return launch_attn_tc<80>(qkv, out, cu_seqlens, n_seq, max_seqlen, heads, scale, total_tokens, workspace, stream);
 }

@@ -96,6 +96,173 @@ MMK_DEV float2 exp2_poly2(float2 x) {
   return e;
 }
 
+
+// ---------------------------------------------------------------------------- per-tile steps
+// (shared by the one-item-per-CTA kernel and the persistent kernel)
+
+// S_t = Q_t K^T for one KV tile (one elected lane issues; Q and K K-major in smem).
+template <int HD, int BKV, int NQ>
+MMK_DEV void issue_s(uint32_t s_tm, uint32_t q_addr, uint32_t k_addr) {
+  using C = TcAttnCfg<HD, BKV, NQ>;
+  constexpr uint32_t idesc_s = umma_idesc_bf16_f32(kTcBQ, BKV);
+  const uint64_t qd = umma_desc_sw128_kmajor(q_addr);
+  const uint64_t kd = umma_desc_sw128_kmajor(k_addr);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) umma_bf16_ss(s_tm, qd + 2 * k, kd + 2 * k, idesc_s, k > 0);
+  if (C::kRem)
+    umma_bf16_ss(s_tm, umma_desc_sw32_kmajor(q_addr + C::kQMain), umma_desc_sw32_kmajor(k_addr + C::kKVMain),
+                 idesc_s, 1u);
+}
+
+// O_t (+)= P_t V for one KV tile: P_t from TMEM (bf16 pairs, 8 columns per 16 keys) as the A
+// operand, V the MN-major B operand (8-row K groups at 128 B main / 32 B remainder per row).
+template <int HD, int BKV, int NQ>
+MMK_DEV void issue_pv(uint32_t o_tm, uint32_t p_tm, uint32_t v_addr, bool first) {
+  using C = TcAttnCfg<HD, BKV, NQ>;
+  constexpr uint32_t idesc_pv_main = umma_idesc_bf16_f32(kTcBQ, 64) | (1u << 16);  // B (V) MN-major
+  constexpr uint32_t idesc_pv_rem = umma_idesc_bf16_f32(kTcBQ, 16) | (1u << 16);
+  constexpr uint32_t kVStepMain = (16 * 128) >> 4, kVStepRem = (16 * 32) >> 4;  // desc units per k-step
+  const uint64_t vd_main = umma_desc_sw128_kmajor(v_addr);              // MN-major, SBO 1024
+  const uint64_t vd_rem = umma_desc_sw32_kmajor(v_addr + C::kKVMain);  // MN-major, SBO 256
+#pragma unroll
+  for (int k = 0; k < BKV / 16; ++k) {
+    const uint32_t acc = (!first || k > 0) ? 1u : 0u;
+    umma_bf16_ts(o_tm, p_tm + 8 * k, vd_main + kVStepMain * k, idesc_pv_main, acc);
+    if (C::kRem) umma_bf16_ts(o_tm + 64, p_tm + 8 * k, vd_rem + kVStepRem * k, idesc_pv_rem, acc);
+  }
+}
+
+// One KV tile of the online softmax for this thread's query row (its TMEM lane): S_t -> registers
+// (then S_t is released to the MMA warp), row max with a lazily updated running max (O_t is
+// rescaled in TMEM only when the max grows by more than 2^8), exponentials -> P_t in TMEM, row
+// sum.  `g` is the tile's index in query tile t's barrier sequence; `first` marks the first KV tile
+// of a work item (no PV of this item precedes it); `valid` = keys of the tile inside the sequence.
+template <int HD, int BKV, int NQ>
+MMK_DEV void softmax_tile(uint32_t s_tm, uint32_t o_tm, uint32_t p_tm, uint64_t* s_full, uint64_t* s_free,
+                          uint64_t* pv_done, uint64_t* p_full, uint32_t g, bool first, int valid, float scale_log2,
+                          float& m_used, float& l, uint32_t lane, bool trace, int t, int j) {
+  (void)trace; (void)t; (void)j;
+  if (trace) { TR(t, j, 0) }
+  mbar_wait(s_full, g & 1);
+  if (trace) { TR(t, j, 1) }
+  tc_fence_after();
+  uint32_t r[BKV];
+#pragma unroll
+  for (int c = 0; c < BKV / 32; ++c) {
+    uint32_t (&rc)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[32 * c]);
+    tmem_ld_32x32b_x32(s_tm + 32 * c, rc);
+  }
+  if constexpr (BKV % 32 != 0) {
+    uint32_t (&rc)[16] = *reinterpret_cast<uint32_t(*)[16]>(&r[BKV - 16]);
+    tmem_ld_32x32b_x16(s_tm + BKV - 16, rc);
+  }
+  tmem_ld_wait();
+  tc_fence_before();
+  __syncwarp();
+  if (lane == 0) mbar_arrive(s_free);  // TMEM S_t may now be overwritten by the next S_t
+  if (trace) { TR(t, j, 2) }
+  if (valid < BKV) {                   // last tile only (uniform branch)
+#pragma unroll
+    for (int i = 0; i < BKV; ++i)
+      if (i >= valid) r[i] = __float_as_uint(-INFINITY);
+  }
+  float mx;
+  {
+    float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+    for (int i = 0; i < BKV; i += 8)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) m4[u] = fmax3(m4[u], __uint_as_float(r[i + 2 * u]), __uint_as_float(r[i + 2 * u + 1]));
+    mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2;
+  }
+  float m_new = m_used, corr = 1.f;
+#ifdef MMK_ATTN_XP_NOMAX  // timing experiment only (make xp): running max from the first tile
+  if (!first) mx = m_used;
+#endif
+  if (mx > m_used + kRescaleThreshold) {
+    m_new = mx;
+    corr = fast_exp2(m_used - m_new);  // 0 on the first tile
+  }
+  if (!first && warp_any(corr != 1.f)) {
+    // rescale O_t once the previous PV_t has retired
+    mbar_wait(pv_done, (g - 1) & 1);
+    tc_fence_after();
+    uint32_t o[16];
+#pragma unroll
+    for (int c = 0; c < HD / 16; ++c) {
+      tmem_ld_32x32b_x16(o_tm + 16 * c, o);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * corr);
+      tmem_st_32x32b_x16(o_tm + 16 * c, o);
+    }
+    tmem_st_wait();
+  }
+  m_used = m_new;
+  // p = 2^(s*scale - m): MMK_POLY8 of every 8 pairs on the FMA pipe (polynomial), the rest on MUFU
+  const float2 sc2 = make_float2(scale_log2, scale_log2);
+  const float2 nm2 = make_float2(-m_new, -m_new);
+  float2 sa = make_float2(0.f, 0.f), sb = make_float2(0.f, 0.f);
+  uint32_t p[BKV / 2];
+#pragma unroll
+  for (int i = 0; i < BKV / 2; ++i) {
+    const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), sc2, nm2);
+    float2 e;
+#ifdef MMK_ATTN_XP_NOEXP  // timing experiment only (make xp): no exponential
+    if (true) {
+      e = x;
+    } else
+#endif
+    if ((i & 7) < MMK_POLY8) {
+      e = exp2_poly2(x);
+    } else {
+      e.x = fast_exp2(x.x);
+      e.y = fast_exp2(x.y);
+    }
+    if (i & 1) sb = __fadd2_rn(sb, e); else sa = __fadd2_rn(sa, e);
+    p[i] = pack_bf16x2(e.x, e.y);
+  }
+  const float sum = (sa.x + sa.y) + (sb.x + sb.y);
+  if (trace) { TR(t, j, 3) }
+  l = l * corr + sum;
+  // P_t -> TMEM (the previous PV_t must have finished reading the buffer; at the first tile of an
+  // item the previous item's last PV retired before its output was read)
+  if (!first) mbar_wait(pv_done, (g - 1) & 1);
+  if (trace) { TR(t, j, 4) }
+  tc_fence_after();
+#pragma unroll
+  for (int c = 0; c < BKV / 64; ++c)
+    tmem_st_32x32b_x32(p_tm + 32 * c, *reinterpret_cast<const uint32_t(*)[32]>(&p[32 * c]));
+  if constexpr ((BKV / 2) % 32 >= 16)
+    tmem_st_32x32b_x16(p_tm + (BKV / 64) * 32, *reinterpret_cast<const uint32_t(*)[16]>(&p[(BKV / 64) * 32]));
+  if constexpr ((BKV / 2) % 16 == 8)
+    tmem_st_32x32b_x8(p_tm + BKV / 2 - 8, *reinterpret_cast<const uint32_t(*)[8]>(&p[BKV / 2 - 8]));
+  tmem_st_wait();
+  tc_fence_before();  // orders the O rescale / P (tcgen05.st) before the arrive
+  __syncwarp();
+  if (lane == 0) mbar_arrive(p_full);
+  if (trace) { TR(t, j, 5) }
+}
+
+// O_t / l -> bf16 output row (16 columns per TMEM load, two 16-byte stores).
+template <int HD>
+MMK_DEV void store_o(uint32_t o_tm, float l, __nv_bfloat16* go, bool row_ok) {
+  const float inv = 1.f / l;
+#pragma unroll
+  for (int c = 0; c < HD / 16; ++c) {
+    uint32_t o[16];
+    tmem_ld_32x32b_x16(o_tm + 16 * c, o);
+    tmem_ld_wait();
+    if (row_ok) {
+      uint32_t w[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w[i] = pack_bf16x2(__uint_as_float(o[2 * i]) * inv, __uint_as_float(o[2 * i + 1]) * inv);
+      st_global_v4(go + 16 * c, w[0], w[1], w[2], w[3]);
+      st_global_v4(go + 16 * c + 8, w[4], w[5], w[6], w[7]);
+    }
+  }
+}
+
 template <int HD, int BKV, int NQ>
 __global__ void __maxnreg__(NQ == 2 ? 168 : 128)
 attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_q_rem,
@@ -190,15 +357,10 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
     // PV_t(j-1) once P_t(j-1) is written.
     const int t = static_cast<int>(warp) - kMmaWarp;
     if (t < n_qt) {
-      constexpr uint32_t idesc_s = umma_idesc_bf16_f32(kTcBQ, BKV);
-      constexpr uint32_t idesc_pv_main = umma_idesc_bf16_f32(kTcBQ, 64) | (1u << 16);  // B (V) MN-major
-      constexpr uint32_t idesc_pv_rem = umma_idesc_bf16_f32(kTcBQ, 16) | (1u << 16);
-      // V as the MN-major B operand: 8-row K groups at 128 B (main) / 32 B (rem) per row
-      constexpr uint32_t kVStepMain = (16 * 128) >> 4, kVStepRem = (16 * 32) >> 4;  // desc units per k-step
       const uint32_t s_tm = tmem + t * BKV;
       const uint32_t o_tm = tmem + C::kOBase + t * HD;
+      const uint32_t p_tm = tmem + C::kPBase + t * C::kPStride;
       const uint32_t q_addr = smem_u32(tile_ptr(C::kQOff + t * C::kQBytes));
-      const uint64_t qd = umma_desc_sw128_kmajor(q_addr);
       mbar_wait(q_full, 0);
       tc_fence_after();
       for (int j = 0; j <= nkv; ++j) {
@@ -210,13 +372,8 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
           tc_fence_after();
           if (t < 2) { TR(2, j, 0) }
           const uint32_t k_addr = smem_u32(tile_ptr(C::kKVOff + st * C::kStageBytes));
-          const uint64_t kd = umma_desc_sw128_kmajor(k_addr);
           if (elect_one()) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) umma_bf16_ss(s_tm, qd + 2 * k, kd + 2 * k, idesc_s, k > 0);
-            if (C::kRem)
-              umma_bf16_ss(s_tm, umma_desc_sw32_kmajor(q_addr + C::kQMain),
-                           umma_desc_sw32_kmajor(k_addr + C::kKVMain), idesc_s, 1u);
+            issue_s<HD, BKV, NQ>(s_tm, q_addr, k_addr);
             umma_commit(&s_full[t]);
           }
           __syncwarp();
@@ -228,17 +385,8 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
           tc_fence_after();
           if (t < 2) { TR(2, j - 1, 3 + t) }
           const uint32_t v_addr = smem_u32(tile_ptr(C::kKVOff + pst * C::kStageBytes + C::kKVBytes));
-          const uint64_t vd_main = umma_desc_sw128_kmajor(v_addr);                 // MN-major, SBO 1024
-          const uint64_t vd_rem = umma_desc_sw32_kmajor(v_addr + C::kKVMain);     // MN-major, SBO 256
           if (elect_one()) {
-            // P_t in TMEM (bf16 pairs, 8 columns per 16 keys): A operand read from tensor memory
-            const uint32_t p_tm = tmem + C::kPBase + t * C::kPStride;
-#pragma unroll
-            for (int k = 0; k < BKV / 16; ++k) {
-              const uint32_t acc = (j > 1 || k > 0) ? 1u : 0u;
-              umma_bf16_ts(o_tm, p_tm + 8 * k, vd_main + kVStepMain * k, idesc_pv_main, acc);
-              if (C::kRem) umma_bf16_ts(o_tm + 64, p_tm + 8 * k, vd_rem + kVStepRem * k, idesc_pv_rem, acc);
-            }
+            issue_pv<HD, BKV, NQ>(o_tm, p_tm, v_addr, j == 1);
             umma_commit(&pv_done[t]);
             umma_commit(&kv_empty[pst]);  // this tile is done with K(j-1), V(j-1)
           }
@@ -256,130 +404,14 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
     const uint32_t o_tm = tmem + C::kOBase + t * HD + lane_base;
     const int row = q0 + t * kTcBQ + q4 * 32 + lane;  // query row within the sequence
     if (t < n_qt) {
+      const uint32_t p_tm = tmem + C::kPBase + t * C::kPStride + lane_base;
       float m_used = -INFINITY, l = 0.f;
-      for (int j = 0; j < nkv; ++j) {
-        if (q4 == 0 && lane == 0 && t < 2) { TR(t, j, 0) }
-        mbar_wait(&s_full[t], j & 1);
-        if (q4 == 0 && lane == 0 && t < 2) { TR(t, j, 1) }
-        tc_fence_after();
-        uint32_t r[BKV];
-#pragma unroll
-        for (int c = 0; c < BKV / 32; ++c) {
-          uint32_t (&rc)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[32 * c]);
-          tmem_ld_32x32b_x32(s_tm + 32 * c, rc);
-        }
-        if constexpr (BKV % 32 != 0) {
-          uint32_t (&rc)[16] = *reinterpret_cast<uint32_t(*)[16]>(&r[BKV - 16]);
-          tmem_ld_32x32b_x16(s_tm + BKV - 16, rc);
-        }
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_free[t]);  // TMEM S_t may now be overwritten by S_t(j+1)
-        if (q4 == 0 && lane == 0 && t < 2) { TR(t, j, 2) }
-        const int valid = len - j * BKV;  // keys of this tile inside the sequence
-        if (valid < BKV) {                // last tile only (uniform branch)
-#pragma unroll
-          for (int i = 0; i < BKV; ++i)
-            if (i >= valid) r[i] = __float_as_uint(-INFINITY);
-        }
-        float mx;
-        {
-          float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-          for (int i = 0; i < BKV; i += 8)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) m4[u] = fmax3(m4[u], __uint_as_float(r[i + 2 * u]), __uint_as_float(r[i + 2 * u + 1]));
-          mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2;
-        }
-        float m_new = m_used, corr = 1.f;
-#ifdef MMK_ATTN_XP_NOMAX  // timing experiment only (make xp): running max from the first tile
-        if (j > 0) mx = m_used;
-#endif
-        if (mx > m_used + kRescaleThreshold) {
-          m_new = mx;
-          corr = fast_exp2(m_used - m_new);  // 0 on the first tile
-        }
-        if (j > 0 && warp_any(corr != 1.f)) {
-          // rescale O_t once PV_t(j-1) has retired
-          mbar_wait(&pv_done[t], (j - 1) & 1);
-          tc_fence_after();
-          uint32_t o[16];
-#pragma unroll
-          for (int c = 0; c < HD / 16; ++c) {
-            tmem_ld_32x32b_x16(o_tm + 16 * c, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * corr);
-            tmem_st_32x32b_x16(o_tm + 16 * c, o);
-          }
-          tmem_st_wait();
-        }
-        m_used = m_new;
-        // p = 2^(s*scale - m): MMK_POLY8 of every 8 pairs on the FMA pipe (polynomial), the rest on MUFU
-        const float2 sc2 = make_float2(scale_log2, scale_log2);
-        const float2 nm2 = make_float2(-m_new, -m_new);
-        float2 sa = make_float2(0.f, 0.f), sb = make_float2(0.f, 0.f);
-        uint32_t p[BKV / 2];
-#pragma unroll
-        for (int i = 0; i < BKV / 2; ++i) {
-          const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), sc2, nm2);
-          float2 e;
-#ifdef MMK_ATTN_XP_NOEXP  // timing experiment only (make xp): no exponential
-          if (true) {
-            e = x;
-          } else
-#endif
-          if ((i & 7) < MMK_POLY8) {
-            e = exp2_poly2(x);
-          } else {
-            e.x = fast_exp2(x.x);
-            e.y = fast_exp2(x.y);
-          }
-          if (i & 1) sb = __fadd2_rn(sb, e); else sa = __fadd2_rn(sa, e);
-          p[i] = pack_bf16x2(e.x, e.y);
-        }
-        const float sum = (sa.x + sa.y) + (sb.x + sb.y);
-        if (q4 == 0 && lane == 0 && t < 2) { TR(t, j, 3) }
-        l = l * corr + sum;
-        // P_t(j) -> TMEM (the PV MMA of tile j-1 must have finished reading the buffer)
-        if (j > 0) mbar_wait(&pv_done[t], (j - 1) & 1);
-        if (q4 == 0 && lane == 0 && t < 2) { TR(t, j, 4) }
-        {
-          tc_fence_after();
-          const uint32_t p_tm = tmem + C::kPBase + t * C::kPStride + lane_base;
-#pragma unroll
-          for (int c = 0; c < BKV / 64; ++c)
-            tmem_st_32x32b_x32(p_tm + 32 * c, *reinterpret_cast<const uint32_t(*)[32]>(&p[32 * c]));
-          if constexpr ((BKV / 2) % 32 >= 16)
-            tmem_st_32x32b_x16(p_tm + (BKV / 64) * 32, *reinterpret_cast<const uint32_t(*)[16]>(&p[(BKV / 64) * 32]));
-          if constexpr ((BKV / 2) % 16 == 8)
-            tmem_st_32x32b_x8(p_tm + BKV / 2 - 8, *reinterpret_cast<const uint32_t(*)[8]>(&p[BKV / 2 - 8]));
-          tmem_st_wait();
-        }
-        tc_fence_before();    // orders the O rescale / P (tcgen05.st) before the arrive
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[t]);
-        if (q4 == 0 && lane == 0 && t < 2) { TR(t, j, 5) }
-      }
+      for (int j = 0; j < nkv; ++j)
+        softmax_tile<HD, BKV, NQ>(s_tm, o_tm, p_tm, &s_full[t], &s_free[t], &pv_done[t], &p_full[t], j, j == 0,
+                                  len - j * BKV, scale_log2, m_used, l, lane, q4 == 0 && lane == 0 && t < 2, t, j);
       mbar_wait(&pv_done[t], (nkv - 1) & 1);
       tc_fence_after();
-      const float inv = 1.f / l;
-      __nv_bfloat16* go = out + static_cast<int64_t>(s_begin + row) * d_model + head * HD;
-#pragma unroll
-      for (int c = 0; c < HD / 16; ++c) {
-        uint32_t o[16];
-        tmem_ld_32x32b_x16(o_tm + 16 * c, o);
-        tmem_ld_wait();
-        if (row < len) {
-          uint32_t w[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            w[i] = pack_bf16x2(__uint_as_float(o[2 * i]) * inv, __uint_as_float(o[2 * i + 1]) * inv);
-          st_global_v4(go + 16 * c, w[0], w[1], w[2], w[3]);
-          st_global_v4(go + 16 * c + 8, w[4], w[5], w[6], w[7]);
-        }
-      }
+      store_o<HD>(o_tm, l, out + static_cast<int64_t>(s_begin + row) * d_model + head * HD, row < len);
     }
   }
 
@@ -389,9 +421,262 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
   if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
 }
 
+
+// ---------------------------------------------------------------------------- persistent form
+// One CTA per SM takes work items — (query block of NQ*128 rows, head, sequence), query block
+// fastest, the heads of one image adjacent — from a global counter, so ragged batches balance
+// dynamically.  The TMA warp fetches and decodes each item and hands it to the other warps
+// through a 4-deep shared-memory ring; every role therefore walks the same item sequence, and the
+// next item's Q (double-buffered) and first K/V tiles load, and its first S = Q K^T runs, while
+// the previous item's last softmax, PV and output store are in flight.  Barrier phases run on
+// counters that continue across items: `kv` (K/V ring), `qi` (Q slot), `g` (KV tiles seen by
+// query tile t), `oi` (items in which tile t was active), `k` (item ring).  An `o_free` handshake
+// keeps the next item's first PV (which overwrites O_t) behind the previous item's output read.
+struct AttnItem {
+  int s_begin, len, q0, head, n_qt, nkv;  // len < 0: no more items
+};
+
 template <int HD, int BKV, int NQ>
+struct TcPersistLayout {
+  using C = TcAttnCfg<HD, BKV, NQ>;
+  static constexpr int kQSlotBytes = NQ * C::kQBytes;
+  static constexpr int kQOff = 0;                          // two Q slots
+  static constexpr int kKVOff = 2 * kQSlotBytes;
+  static constexpr int kBarOff = kKVOff + C::STAGES * C::kStageBytes;
+  static constexpr int kSmem = kBarOff + 512 + 1024;
+  static_assert((12 + 3 * C::STAGES + 5 * NQ) * 8 + 4 * sizeof(AttnItem) + 4 <= 512, "barrier area");
+  static_assert(kSmem <= 232448, "shared memory overflow");
+};
+
+template <int HD, int BKV, int NQ>
+__global__ void __maxnreg__(NQ == 2 ? 168 : 128)
+attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_q_rem,
+                       const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_kv_rem,
+                       __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ cu_seqlens, int n_seq,
+                       int heads, int qblocks, float scale_log2, int* __restrict__ item_counter) {
+  using C = TcAttnCfg<HD, BKV, NQ>;
+  using Lay = TcPersistLayout<HD, BKV, NQ>;
+  constexpr int kTmaWarp = 4 * NQ, kMmaWarp = 4 * NQ + 1;  // MMA warp of query tile t: kMmaWarp + t
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::kBarOff);
+  uint64_t* q_full = bars + 0;                 // [2] Q slot loaded
+  uint64_t* q_empty = bars + 2;                // [2] every MMA warp is done with the Q slot
+  uint64_t* k_full = bars + 4;                 // [STAGES]
+  uint64_t* v_full = k_full + C::STAGES;       // [STAGES]
+  uint64_t* kv_empty = v_full + C::STAGES;     // [STAGES]
+  uint64_t* s_full = kv_empty + C::STAGES;     // [NQ]
+  uint64_t* s_free = s_full + NQ;              // [NQ]
+  uint64_t* p_full = s_free + NQ;              // [NQ]
+  uint64_t* pv_done = p_full + NQ;             // [NQ]
+  uint64_t* o_free = pv_done + NQ;             // [NQ] softmax -> MMA: O_t read out
+  uint64_t* item_full = o_free + NQ;           // [4] work-item ring: item published
+  uint64_t* item_empty = item_full + 4;        // [4] every consumer warp has copied it
+  AttnItem* ring = reinterpret_cast<AttnItem*>(item_empty + 4);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + 4);
+
+  const int n_items = qblocks * heads * n_seq;
+  const int d_model = heads * HD;
+  const uint32_t warp = warp_id_uniform();
+  const uint32_t lane = lane_id();
+
+  if (warp == kTmaWarp && lane == 0) {
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_kv);
+    if (C::kRem) {
+      tma_prefetch_desc(&tm_q_rem);
+      tma_prefetch_desc(&tm_kv_rem);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&q_full[b], 1);
+      mbar_init(&q_empty[b], NQ);
+    }
+    for (int st = 0; st < C::STAGES; ++st) {
+      mbar_init(&k_full[st], 1);
+      mbar_init(&v_full[st], 1);
+      mbar_init(&kv_empty[st], NQ);  // one release per query tile's MMA warp (inactive ones too)
+    }
+    for (int t = 0; t < NQ; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&s_free[t], 4);
+      mbar_init(&p_full[t], 4);
+      mbar_init(&pv_done[t], 1);
+      mbar_init(&o_free[t], 4);
+    }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&item_full[i], 1);
+      mbar_init(&item_empty[i], 5 * NQ);  // MMA warps + softmax warps
+    }
+    fence_barrier_init();
+  }
+  if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  auto tile_ptr = [&](int off) { return smem + off; };
+  // consumer side of the ring: copy item k, release its slot
+  auto next_item = [&](uint32_t& k) -> AttnItem {
+    const int slot = k & 3;
+    mbar_wait(&item_full[slot], (k >> 2) & 1);
+    const volatile AttnItem* e = ring + slot;
+    AttnItem it{e->s_begin, e->len, e->q0, e->head, e->n_qt, e->nkv};
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&item_empty[slot]);
+    ++k;
+    return it;
+  };
+
+  if (warp == kTmaWarp) {
+    // ---------------------------------------------------------------- scheduler + TMA producer
+    if (elect_one()) {
+      uint32_t kv = 0, qi = 0;
+      for (uint32_t k = 0;; ++k) {
+        const int item = atomicAdd(item_counter, 1);
+        AttnItem it{0, -1, 0, 0, 0, 0};
+        if (item < n_items) {
+          const int qb = item % qblocks, rest = item / qblocks;
+          it.head = rest % heads;
+          const int seq = rest / heads;
+          it.s_begin = __ldg(cu_seqlens + seq);
+          it.len = __ldg(cu_seqlens + seq + 1) - it.s_begin;
+          it.q0 = qb * NQ * kTcBQ;
+          it.n_qt = it.q0 < it.len ? min(NQ, (it.len - it.q0 + kTcBQ - 1) / kTcBQ) : 0;  // 0: empty item
+          it.nkv = (it.len + BKV - 1) / BKV;
+        }
+        const int slot_i = k & 3;
+        mbar_wait(&item_empty[slot_i], ((k >> 2) & 1) ^ 1);
+        volatile AttnItem* e = ring + slot_i;
+        e->s_begin = it.s_begin; e->len = it.len; e->q0 = it.q0; e->head = it.head; e->n_qt = it.n_qt; e->nkv = it.nkv;
+        mbar_arrive(&item_full[slot_i]);  // release: the item is visible to the waiting warps
+        if (it.len < 0) break;
+        if (it.n_qt == 0) continue;
+        const int col_q = it.head * HD, col_k = d_model + it.head * HD, col_v = 2 * d_model + it.head * HD;
+        const int qs = qi & 1;
+        mbar_wait(&q_empty[qs], ((qi >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[qs], it.n_qt * C::kQBytes);
+        for (int t = 0; t < it.n_qt; ++t) {
+          uint8_t* q = tile_ptr(Lay::kQOff + qs * Lay::kQSlotBytes + t * C::kQBytes);
+          const int row = it.s_begin + it.q0 + t * kTcBQ;
+          tma_load_2d(&tm_q, &q_full[qs], q, col_q, row);
+          if (C::kRem) tma_load_2d(&tm_q_rem, &q_full[qs], q + C::kQMain, col_q + 64, row);
+        }
+        ++qi;
+        for (int j = 0; j < it.nkv; ++j, ++kv) {
+          const int st = kv % C::STAGES;
+          mbar_wait(&kv_empty[st], ((kv / C::STAGES) & 1) ^ 1);
+          uint8_t* kt = tile_ptr(Lay::kKVOff + st * C::kStageBytes);
+          uint8_t* vt = kt + C::kKVBytes;
+          const int row = it.s_begin + j * BKV;
+          mbar_arrive_expect_tx(&k_full[st], C::kKVBytes);
+          tma_load_2d(&tm_kv, &k_full[st], kt, col_k, row);
+          if (C::kRem) tma_load_2d(&tm_kv_rem, &k_full[st], kt + C::kKVMain, col_k + 64, row);
+          mbar_arrive_expect_tx(&v_full[st], C::kKVBytes);
+          tma_load_2d(&tm_kv, &v_full[st], vt, col_v, row);
+          if (C::kRem) tma_load_2d(&tm_kv_rem, &v_full[st], vt + C::kKVMain, col_v + 64, row);
+        }
+      }
+    }
+  } else if (warp > kTmaWarp) {
+    // ---------------------------------------------------------------- MMA issuers
+    const int t = static_cast<int>(warp) - kMmaWarp;
+    const uint32_t s_tm = tmem + t * BKV;
+    const uint32_t o_tm = tmem + C::kOBase + t * HD;
+    const uint32_t p_tm = tmem + C::kPBase + t * C::kPStride;
+    uint32_t kv = 0, qi = 0, g = 0, oi = 0, k = 0;
+    for (;;) {
+      const AttnItem it = next_item(k);
+      if (it.len < 0) break;
+      if (it.n_qt == 0) continue;
+      const int qs = qi & 1;
+      const uint32_t q_phase = (qi >> 1) & 1;
+      ++qi;
+      if (t >= it.n_qt) {  // inactive in this item: keep the K/V ring and Q slot accounting
+        for (int j = 0; j < it.nkv; ++j, ++kv) {
+          const int st = kv % C::STAGES;
+          mbar_wait(&k_full[st], (kv / C::STAGES) & 1);  // never run ahead of the ring's phase
+          if (elect_one()) mbar_arrive(&kv_empty[st]);
+          __syncwarp();
+        }
+        if (elect_one()) mbar_arrive(&q_empty[qs]);
+        __syncwarp();
+        continue;
+      }
+      const uint32_t q_addr = smem_u32(tile_ptr(Lay::kQOff + qs * Lay::kQSlotBytes + t * C::kQBytes));
+      mbar_wait(&q_full[qs], q_phase);
+      tc_fence_after();
+      for (int j = 0; j <= it.nkv; ++j) {
+        if (j < it.nkv) {
+          const uint32_t kvj = kv + j;
+          const int st = kvj % C::STAGES;
+          mbar_wait(&k_full[st], (kvj / C::STAGES) & 1);
+          if (g + j > 0) mbar_wait(&s_free[t], (g + j - 1) & 1);
+          tc_fence_after();
+          const uint32_t k_addr = smem_u32(tile_ptr(Lay::kKVOff + st * C::kStageBytes));
+          if (elect_one()) {
+            issue_s<HD, BKV, NQ>(s_tm, q_addr, k_addr);
+            umma_commit(&s_full[t]);
+            if (j == it.nkv - 1) umma_commit(&q_empty[qs]);  // last read of this item's Q
+          }
+          __syncwarp();
+        }
+        if (j > 0) {
+          const uint32_t kvp = kv + j - 1;
+          const int pst = kvp % C::STAGES;
+          mbar_wait(&v_full[pst], (kvp / C::STAGES) & 1);
+          mbar_wait(&p_full[t], (g + j - 1) & 1);
+          if (j == 1 && oi > 0) mbar_wait(&o_free[t], (oi - 1) & 1);  // previous item's O_t read out
+          tc_fence_after();
+          const uint32_t v_addr = smem_u32(tile_ptr(Lay::kKVOff + pst * C::kStageBytes + C::kKVBytes));
+          if (elect_one()) {
+            issue_pv<HD, BKV, NQ>(o_tm, p_tm, v_addr, j == 1);
+            umma_commit(&pv_done[t]);
+            umma_commit(&kv_empty[pst]);
+          }
+          __syncwarp();
+        }
+      }
+      kv += it.nkv;
+      g += it.nkv;
+      ++oi;
+    }
+  } else {
+    // ---------------------------------------------------------------- softmax warpgroups
+    const int t = warp >> 2;
+    const uint32_t q4 = warp & 3;
+    const uint32_t lane_base = (q4 * 32u) << 16;
+    const uint32_t s_tm = tmem + t * BKV + lane_base;
+    const uint32_t o_tm = tmem + C::kOBase + t * HD + lane_base;
+    const uint32_t p_tm = tmem + C::kPBase + t * C::kPStride + lane_base;
+    uint32_t g = 0, k = 0;
+    for (;;) {
+      const AttnItem it = next_item(k);
+      if (it.len < 0) break;
+      if (t >= it.n_qt) continue;  // also skips empty items (n_qt == 0)
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < it.nkv; ++j)
+        softmax_tile<HD, BKV, NQ>(s_tm, o_tm, p_tm, &s_full[t], &s_free[t], &pv_done[t], &p_full[t], g + j, j == 0,
+                                  it.len - j * BKV, scale_log2, m_used, l, lane, false, t, j);
+      g += it.nkv;
+      mbar_wait(&pv_done[t], (g - 1) & 1);
+      tc_fence_after();
+      const int row = it.q0 + t * kTcBQ + q4 * 32 + lane;
+      store_o<HD>(o_tm, l, out + static_cast<int64_t>(it.s_begin + row) * d_model + it.head * HD, row < it.len);
+      tc_fence_before();  // O_t reads complete before the next item's first PV overwrites it
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_free[t]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
+}
+
+template <int HD, int BKV, int NQ, bool PERSIST>
 static int launch_attn_cfg(const void* qkv, void* out, const int32_t* cu, int n_seq, int max_s, int heads,
-                           float scale, int64_t total_rows, cudaStream_t stream) {
+                           float scale, int64_t total_rows, void* workspace, cudaStream_t stream) {
   using C = TcAttnCfg<HD, BKV, NQ>;
   const uint64_t ld = 3ull * heads * HD;
   const uint64_t dims[2] = {ld, static_cast<uint64_t>(total_rows)};
@@ -404,13 +689,31 @@ static int launch_attn_cfg(const void* qkv, void* out, const int32_t* cu, int n_
   if (!rc && C::kRem) rc = make_tmap_bf16(&tkvr, qkv, 2, dims, strides, bkvr, CU_TENSOR_MAP_SWIZZLE_32B);
   if (rc) return rc;
   if (!C::kRem) { tqr = tq; tkvr = tkv; }
-  static std::atomic<uint64_t> attr_done{0};
-  rc = ensure_smem_attr(reinterpret_cast<const void*>(attn_fwd_tc<HD, BKV, NQ>), C::kSmem, attr_done,
-                        "attention_tc: cudaFuncSetAttribute");
-  if (rc) return rc;
-  dim3 grid((max_s + NQ * kTcBQ - 1) / (NQ * kTcBQ), heads, n_seq);
-  attn_fwd_tc<HD, BKV, NQ><<<grid, C::kThreads, C::kSmem, stream>>>(
-      tq, tqr, tkv, tkvr, reinterpret_cast<__nv_bfloat16*>(out), cu, heads, scale * 1.4426950408889634f);
+  const float scale_log2 = scale * 1.4426950408889634f;
+  const int qblocks = (max_s + NQ * kTcBQ - 1) / (NQ * kTcBQ);
+  __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out);
+  if constexpr (PERSIST) {
+    using Lay = TcPersistLayout<HD, BKV, NQ>;
+    const int64_t n_items = static_cast<int64_t>(qblocks) * heads * n_seq;
+    if (n_items >= INT32_MAX) return set_error(MMK_ERR_UNSUPPORTED, "attention_tc: too many work items");
+    static std::atomic<uint64_t> attr_done{0};
+    rc = ensure_smem_attr(reinterpret_cast<const void*>(attn_fwd_tc_persistent<HD, BKV, NQ>), Lay::kSmem, attr_done,
+                          "attention_tc: cudaFuncSetAttribute");
+    if (rc) return rc;
+    cudaError_t me = cudaMemsetAsync(workspace, 0, sizeof(int), stream);  // work-item counter
+    if (me != cudaSuccess) return set_cuda_error(me, "attention_tc: workspace reset");
+    const int grid = static_cast<int>(n_items < num_sms() ? n_items : num_sms());  // one CTA per SM
+    attn_fwd_tc_persistent<HD, BKV, NQ><<<grid, C::kThreads, Lay::kSmem, stream>>>(
+        tq, tqr, tkv, tkvr, o, cu, n_seq, heads, qblocks, scale_log2, reinterpret_cast<int*>(workspace));
+  } else {
+    static std::atomic<uint64_t> attr_done{0};
+    rc = ensure_smem_attr(reinterpret_cast<const void*>(attn_fwd_tc<HD, BKV, NQ>), C::kSmem, attr_done,
+                          "attention_tc: cudaFuncSetAttribute");
+    if (rc) return rc;
+    if (n_seq > 65535 || heads > 65535) return set_error(MMK_ERR_UNSUPPORTED, "attention: too many sequences/heads");
+    attn_fwd_tc<HD, BKV, NQ><<<dim3(qblocks, heads, n_seq), C::kThreads, C::kSmem, stream>>>(
+        tq, tqr, tkv, tkvr, o, cu, heads, scale_log2);
+  }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "attention_tc: launch");
 }
@@ -419,15 +722,27 @@ static int launch_attn_cfg(const void* qkv, void* out, const int32_t* cu, int n_
 // TMEM (A operand of the PV MMA read from tensor memory), which needs S + O + P <= 512 columns:
 //   hd 80: 2 query tiles, 112-key tiles:  S 2x112 + O 2x80 + P 2x56 (aligned)  = 504 columns
 //   hd 64: 3 query tiles,  64-key tiles:  S 3x64  + O 3x64 + P 3x32           = 480 columns
+//   hd 64 runs persistent when there are more than two waves of work items (short CLIP / ViT
+//   sequences: each item's prologue and epilogue overlap its neighbours; a single partial wave is
+//   faster without the scheduler); hd 80 one item per CTA (its softmax sits at the 168-register
+//   cap, where the persistent loop state spills).  MMK_ATTN_PERSIST=0/1 overrides for A/B runs.
 template <int HD>
 int launch_attn_tc(const void* qkv, void* out, const int32_t* cu, int n_seq, int max_s, int heads, float scale,
-                   int64_t total_rows, cudaStream_t stream) {
-  if constexpr (HD == 64) return launch_attn_cfg<HD, 64, 3>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, stream);
-  else return launch_attn_cfg<HD, 112, 2>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, stream);
+                   int64_t total_rows, void* workspace, cudaStream_t stream) {
+  static const int force = [] {
+    const char* e = getenv("MMK_ATTN_PERSIST");
+    return e ? atoi(e) : -1;
+  }();
+  constexpr int BKV = HD == 64 ? 64 : 112, NQ = HD == 64 ? 3 : 2;
+  const int64_t items = static_cast<int64_t>((max_s + NQ * kTcBQ - 1) / (NQ * kTcBQ)) * heads * n_seq;
+  const bool persist = force == 1 || (force != 0 && HD == 64 && items > 2 * num_sms());
+  if (persist)
+    return launch_attn_cfg<HD, BKV, NQ, true>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, workspace, stream);
+  return launch_attn_cfg<HD, BKV, NQ, false>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, workspace, stream);
 }
 
-template int launch_attn_tc<64>(const void*, void*, const int32_t*, int, int, int, float, int64_t, cudaStream_t);
-template int launch_attn_tc<80>(const void*, void*, const int32_t*, int, int, int, float, int64_t, cudaStream_t);
+template int launch_attn_tc<64>(const void*, void*, const int32_t*, int, int, int, float, int64_t, void*, cudaStream_t);
+template int launch_attn_tc<80>(const void*, void*, const int32_t*, int, int, int, float, int64_t, void*, cudaStream_t);
 
 }  // namespace mmk
 

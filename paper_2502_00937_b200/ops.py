@@ -172,6 +172,9 @@ def _attn_flops(cu_seqlens, heads, head_dim):
     return _SEQ_FLOPS.get(cu_seqlens.data_ptr(), 0.0) * heads * head_dim
 
 
+_ATTN_WS_BYTES = int(_lib.lib.mmk_attention_workspace_size())
+
+
 def attention(qkv, cu_seqlens, n_seq: int, max_seqlen: int, heads: int, head_dim: int, out=None,
               scale: float | None = None):
     T = qkv.shape[0]
@@ -179,9 +182,11 @@ def attention(qkv, cu_seqlens, n_seq: int, max_seqlen: int, heads: int, head_dim
         out = torch.empty(T, heads * head_dim, dtype=torch.bfloat16, device=qkv.device)
     if scale is None:
         scale = head_dim ** -0.5
+    # per-call workspace (the persistent kernel's work-item counter; stream-ordered by the allocator)
+    ws = torch.empty(_ATTN_WS_BYTES, dtype=torch.uint8, device=qkv.device)
     _t0 = _begin()
     _lib.check(_lib.lib.mmk_attention_varlen_bf16(qkv.data_ptr(), out.data_ptr(), cu_seqlens.data_ptr(), n_seq,
-                                                  max_seqlen, T, heads, head_dim, float(scale), _s()))
+                                                  max_seqlen, T, heads, head_dim, float(scale), ws.data_ptr(), _s()))
     _end('attention', _attn_flops(cu_seqlens, heads, head_dim), _t0)
     return out
 

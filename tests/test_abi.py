@@ -14,7 +14,7 @@ LIB = ROOT / "paper_2502_00937_b200" / "libmmk.so"
 
 def declared_symbols():
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(mmk_\w+)\s*\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(mmk_\w+)\s*\(", text, flags=re.M)))
 
 
 def test_header_declares_the_path():
@@ -41,7 +41,7 @@ def test_argument_errors_map_to_reference_exceptions():
     rc = _lib.lib.mmk_tile_plan(None, None, -1, 560, 1601, 4, 0, 0, None, None, None, None, None, None, None)
     with pytest.raises(SpecError):
         _lib.check(rc)
-    rc = _lib.lib.mmk_attention_varlen_bf16(None, None, None, 1, 16, 16, 16, 72, 0.1, None)
+    rc = _lib.lib.mmk_attention_varlen_bf16(None, None, None, 1, 16, 16, 16, 72, 0.1, None, None)
     with pytest.raises(_lib.ProfileError):
         _lib.check(rc)
     rc = _lib.lib.mmk_gemm_bf16(None, 64, None, 64, 128, 100, 64, 0, None, None, 100, 1.0, None, 0, None)
