@@ -520,7 +520,11 @@ attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_co
     const int slot = k & 3;
     mbar_wait(&item_full[slot], (k >> 2) & 1);
     const volatile AttnItem* e = ring + slot;
-    AttnItem it{e->s_begin, e->len, e->q0, e->head, e->n_qt, e->nkv};
+    // broadcast from lane 0 so the fields are provably warp-uniform (uniform registers, not the
+    // vector registers the softmax loop needs)
+    AttnItem it{__shfl_sync(0xffffffffu, e->s_begin, 0), __shfl_sync(0xffffffffu, e->len, 0),
+                __shfl_sync(0xffffffffu, e->q0, 0), __shfl_sync(0xffffffffu, e->head, 0),
+                __shfl_sync(0xffffffffu, e->n_qt, 0), __shfl_sync(0xffffffffu, e->nkv, 0)};
     __syncwarp();
     if (lane == 0) mbar_arrive(&item_empty[slot]);
     ++k;
