@@ -204,8 +204,7 @@ MMK_DEV void softmax_tile(uint32_t s_tm, uint32_t o_tm, uint32_t p_tm, uint64_t*
   const float2 nm2 = make_float2(-m_new, -m_new);
   float2 sa = make_float2(0.f, 0.f), sb = make_float2(0.f, 0.f);
   uint32_t p[BKV / 2];
-#pragma unroll
-  for (int i = 0; i < BKV / 2; ++i) {
+  auto exp_pair = [&](int i) {
     const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), sc2, nm2);
     float2 e;
 #ifdef MMK_ATTN_XP_NOEXP  // timing experiment only (make xp): no exponential
@@ -221,6 +220,23 @@ MMK_DEV void softmax_tile(uint32_t s_tm, uint32_t o_tm, uint32_t p_tm, uint64_t*
     }
     if (i & 1) sb = __fadd2_rn(sb, e); else sa = __fadd2_rn(sa, e);
     p[i] = pack_bf16x2(e.x, e.y);
+  };
+  if (valid >= BKV) {
+#pragma unroll
+    for (int i = 0; i < BKV / 2; ++i) exp_pair(i);
+  } else {
+    // last tile of the sequence: 16-key groups entirely past its end get P = 0 without any
+    // exponential (uniform branch per group)
+#pragma unroll
+    for (int g16 = 0; g16 < BKV / 16; ++g16) {
+      if (16 * g16 < valid) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) exp_pair(8 * g16 + k);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) p[8 * g16 + k] = 0u;
+      }
+    }
   }
   const float sum = (sa.x + sa.y) + (sb.x + sb.y);
   if (trace) { TR(t, j, 3) }
