@@ -6,12 +6,18 @@
 // pkg/src/lmmsim/profiles.py:136-145) with the encoder's real dense contractions:
 // patch-embed (K2), QKV (K4), O-proj + residual (K6), FC1 + GELU (K7), FC2 + residual (K8).
 //
-// Structure (one CTA per SM, persistent over output tiles):
+// Two kernels share the structure (persistent over output tiles, warp-specialised):
 //   warp 0      TMA producer: A/B k-blocks -> STAGES-deep smem ring (128B swizzle)
-//   warp 1      MMA issuer:   one thread issues tcgen05.mma (M=128, N=BN, K=16) into TMEM
-//   warp 2      TMEM allocator (2 x BN fp32 columns: double-buffered accumulator)
+//   warp 1      MMA issuer:   one elected thread issues tcgen05.mma into TMEM
+//   warp 2      TMEM allocator (double-buffered fp32 accumulator)
 //   warps 4..11 epilogue:     tcgen05.ld -> bias / activation / gated residual -> global
 // Epilogue of tile i overlaps the MMAs of tile i+1 via the two accumulator buffers.
+//   gemm_bf16_tcgen05      one CTA per SM, 128 x BN tiles, M=128 MMAs (small or odd-N problems)
+//   gemm_bf16_tcgen05_2sm  CTA pairs (clusters of 2, one TPC): 256 x 256 tiles with
+//                          tcgen05.mma.cta_group::2 (M=256), each CTA loading its 128 rows of A
+//                          and half of B, completions counted on the leader CTA's barriers;
+//                          bf16 outputs leave through 128B-swizzled smem + TMA stores, the fp32
+//                          residual streams through a 2-slot TMA ring per epilogue warp.
 #include "sm100_common.cuh"
 #include <cstdlib>
 #include "mmk_internal.h"
