@@ -36,8 +36,14 @@ __device__ long long g_attn_trace[3][64][8];
 #define TR(role, j, ev)
 #endif
 
+// Pairs out of every 8 whose exp2 runs as an FMA-pipe polynomial (the rest on MUFU): 2 for the
+// exact softmax, 1 for the speculative one, whose missing max pass leaves less FMA/ALU work to
+// interleave with MUFU (measured, profiles/r01_attention.md).
 #ifndef MMK_POLY8
-#define MMK_POLY8 2  // pairs out of every 8 whose exp2 runs as an FMA-pipe polynomial
+#define MMK_POLY8 2
+#endif
+#ifndef MMK_POLY8_SPEC
+#define MMK_POLY8_SPEC 1
 #endif
 
 constexpr int kTcBQ = 128;
@@ -82,6 +88,8 @@ MMK_DEV float fmax3(float a, float b, float c) {
 // 2^x for a pair on the FMA pipe: round-to-nearest split x = n + f (magic-number trick),
 // degree-3 polynomial for 2^f on [-0.5, 0.5] (max rel err 1.0e-4, far below bf16's 2^-8), and
 // the exponent added in the integer domain.  x is clamped at -126 (masked -inf -> ~0).
+// (x > 127 wraps the exponent: the speculative softmax tracks the largest polynomial input and
+// sends such rows to the exact pass.)
 MMK_DEV float2 exp2_poly2(float2 x) {
   constexpr float kMagic = 12582912.f;  // 1.5 * 2^23
   x.x = fmaxf(x.x, -126.f);
@@ -141,7 +149,12 @@ MMK_DEV void issue_pv(uint32_t o_tm, uint32_t p_tm, uint32_t v_addr, bool first)
 // rescaled in TMEM only when the max grows by more than 2^8), exponentials -> P_t in TMEM, row
 // sum.  `g` is the tile's index in query tile t's barrier sequence; `first` marks the first KV tile
 // of a work item (no PV of this item precedes it); `valid` = keys of the tile inside the sequence.
-template <int HD, int BKV, int NQ>
+//
+// SPEC (speculative max): only an item's first tile computes a row max; every later tile reuses
+// it without a max pass or rescale.  P = 2^(x - m) may then exceed 1 by any factor — harmless in
+// bf16 P / fp32 O and l up to ~2^100 — and a row whose scores outgrow the first tile's by more
+// than that ends with l > 2^100 or inf; the caller flags it and the launch is redone exactly.
+template <int HD, int BKV, int NQ, bool SPEC = false>
 MMK_DEV void softmax_tile(uint32_t s_tm, uint32_t o_tm, uint32_t p_tm, uint64_t* s_full, uint64_t* s_free,
                           uint64_t* pv_done, uint64_t* p_full, uint32_t g, bool first, int valid, float scale_log2,
                           float& m_used, float& l, uint32_t lane, bool trace, int t, int j) {
@@ -170,24 +183,20 @@ MMK_DEV void softmax_tile(uint32_t s_tm, uint32_t o_tm, uint32_t p_tm, uint64_t*
     for (int i = 0; i < BKV; ++i)
       if (i >= valid) r[i] = __float_as_uint(-INFINITY);
   }
-  float mx;
-  {
+  float m_new = m_used, corr = 1.f;
+  if (!SPEC || first) {
     float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
     for (int i = 0; i < BKV; i += 8)
 #pragma unroll
       for (int u = 0; u < 4; ++u) m4[u] = fmax3(m4[u], __uint_as_float(r[i + 2 * u]), __uint_as_float(r[i + 2 * u + 1]));
-    mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2;
+    const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * scale_log2;
+    if (mx > m_used + kRescaleThreshold) {
+      m_new = mx;
+      corr = fast_exp2(m_used - m_new);  // 0 on the first tile
+    }
   }
-  float m_new = m_used, corr = 1.f;
-#ifdef MMK_ATTN_XP_NOMAX  // timing experiment only (make xp): running max from the first tile
-  if (!first) mx = m_used;
-#endif
-  if (mx > m_used + kRescaleThreshold) {
-    m_new = mx;
-    corr = fast_exp2(m_used - m_new);  // 0 on the first tile
-  }
-  if (!first && warp_any(corr != 1.f)) {
+  if (!SPEC && !first && warp_any(corr != 1.f)) {
     // rescale O_t once the previous PV_t has retired
     mbar_wait(pv_done, (g - 1) & 1);
     tc_fence_after();
@@ -203,10 +212,11 @@ MMK_DEV void softmax_tile(uint32_t s_tm, uint32_t o_tm, uint32_t p_tm, uint64_t*
     tmem_st_wait();
   }
   m_used = m_new;
-  // p = 2^(s*scale - m): MMK_POLY8 of every 8 pairs on the FMA pipe (polynomial), the rest on MUFU
+  // p = 2^(s*scale - m): MMK_POLY8(_SPEC) of every 8 pairs on the FMA pipe (polynomial), the rest on MUFU
   const float2 sc2 = make_float2(scale_log2, scale_log2);
   const float2 nm2 = make_float2(-m_new, -m_new);
   float2 sa = make_float2(0.f, 0.f), sb = make_float2(0.f, 0.f);
+  float pm = -INFINITY;  // SPEC: largest polynomial input (the polynomial is valid up to 127)
   uint32_t p[BKV / 2];
   auto exp_pair = [&](int i) {
     const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), sc2, nm2);
@@ -216,7 +226,8 @@ MMK_DEV void softmax_tile(uint32_t s_tm, uint32_t o_tm, uint32_t p_tm, uint64_t*
       e = x;
     } else
 #endif
-    if ((i & 7) < MMK_POLY8) {
+    if ((i & 7) < (SPEC ? MMK_POLY8_SPEC : MMK_POLY8)) {
+      if constexpr (SPEC) pm = fmax3(pm, x.x, x.y);
       e = exp2_poly2(x);
     } else {
       e.x = fast_exp2(x.x);
@@ -242,7 +253,10 @@ MMK_DEV void softmax_tile(uint32_t s_tm, uint32_t o_tm, uint32_t p_tm, uint64_t*
       }
     }
   }
-  const float sum = (sa.x + sa.y) + (sb.x + sb.y);
+  float sum = (sa.x + sa.y) + (sb.x + sb.y);
+  if constexpr (SPEC) {
+    if (pm > 126.f) sum = INFINITY;  // wrapped polynomial: route the row to the exact pass
+  }
   if (trace) { TR(t, j, 3) }
   l = l * corr + sum;
   // P_t -> TMEM (the previous PV_t must have finished reading the buffer; at the first tile of an
@@ -264,6 +278,13 @@ MMK_DEV void softmax_tile(uint32_t s_tm, uint32_t o_tm, uint32_t p_tm, uint64_t*
   if (trace) { TR(t, j, 5) }
 }
 
+// Speculative softmax: a row whose l left the safe range (scores outgrew the first tile's max by
+// more than ~2^100) marks the launch for the exact pass.
+constexpr float kSpecLimit = 1.2676506e30f;  // 2^100
+MMK_DEV void flag_overflow(float l, int* flag) {
+  if (!(l <= kSpecLimit)) *reinterpret_cast<volatile int*>(flag) = 1;  // also catches inf / NaN
+}
+
 // O_t / l -> bf16 output row (16 columns per TMEM load, two 16-byte stores).
 template <int HD>
 MMK_DEV void store_o(uint32_t o_tm, float l, __nv_bfloat16* go, bool row_ok) {
@@ -283,11 +304,12 @@ MMK_DEV void store_o(uint32_t o_tm, float l, __nv_bfloat16* go, bool row_ok) {
   }
 }
 
-template <int HD, int BKV, int NQ>
+template <int HD, int BKV, int NQ, bool SPEC>
 __global__ void __maxnreg__(NQ == 2 ? 168 : 128)
 attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_q_rem,
             const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_kv_rem,
-            __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ cu_seqlens, int heads, float scale_log2) {
+            __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ cu_seqlens, int heads, float scale_log2,
+            int* __restrict__ overflow_flag) {
   using C = TcAttnCfg<HD, BKV, NQ>;
   constexpr int kTmaWarp = 4 * NQ, kMmaWarp = 4 * NQ + 1;  // MMA warp of query tile t: kMmaWarp + t
   extern __shared__ uint8_t smem_raw[];
@@ -427,10 +449,12 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
       const uint32_t p_tm = tmem + C::kPBase + t * C::kPStride + lane_base;
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < nkv; ++j)
-        softmax_tile<HD, BKV, NQ>(s_tm, o_tm, p_tm, &s_full[t], &s_free[t], &pv_done[t], &p_full[t], j, j == 0,
-                                  len - j * BKV, scale_log2, m_used, l, lane, q4 == 0 && lane == 0 && t < 2, t, j);
+        softmax_tile<HD, BKV, NQ, SPEC>(s_tm, o_tm, p_tm, &s_full[t], &s_free[t], &pv_done[t], &p_full[t], j, j == 0,
+                                        len - j * BKV, scale_log2, m_used, l, lane, q4 == 0 && lane == 0 && t < 2, t,
+                                        j);
       mbar_wait(&pv_done[t], (nkv - 1) & 1);
       tc_fence_after();
+      if constexpr (SPEC) flag_overflow(l, overflow_flag);
       store_o<HD>(o_tm, l, out + static_cast<int64_t>(s_begin + row) * d_model + head * HD, row < len);
     }
   }
@@ -468,12 +492,16 @@ struct TcPersistLayout {
   static_assert(kSmem <= 232448, "shared memory overflow");
 };
 
-template <int HD, int BKV, int NQ>
+// `gate`: when non-null the launch is the exact redo of a speculative pass and exits at once
+// unless that pass flagged an overflow.
+template <int HD, int BKV, int NQ, bool SPEC>
 __global__ void __maxnreg__(NQ == 2 ? 168 : 128)
 attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_q_rem,
                        const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_kv_rem,
                        __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ cu_seqlens, int n_seq,
-                       int heads, int qblocks, float scale_log2, int* __restrict__ item_counter) {
+                       int heads, int qblocks, float scale_log2, int* __restrict__ item_counter,
+                       int* __restrict__ overflow_flag, const int* __restrict__ gate) {
+  if (gate != nullptr && *reinterpret_cast<const volatile int*>(gate) == 0) return;
   using C = TcAttnCfg<HD, BKV, NQ>;
   using Lay = TcPersistLayout<HD, BKV, NQ>;
   constexpr int kTmaWarp = 4 * NQ, kMmaWarp = 4 * NQ + 1;  // MMA warp of query tile t: kMmaWarp + t
@@ -679,11 +707,12 @@ attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       if (t >= it.n_qt) continue;  // also skips empty items (n_qt == 0)
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < it.nkv; ++j)
-        softmax_tile<HD, BKV, NQ>(s_tm, o_tm, p_tm, &s_full[t], &s_free[t], &pv_done[t], &p_full[t], g + j, j == 0,
-                                  it.len - j * BKV, scale_log2, m_used, l, lane, false, t, j);
+        softmax_tile<HD, BKV, NQ, SPEC>(s_tm, o_tm, p_tm, &s_full[t], &s_free[t], &pv_done[t], &p_full[t], g + j,
+                                        j == 0, it.len - j * BKV, scale_log2, m_used, l, lane, false, t, j);
       g += it.nkv;
       mbar_wait(&pv_done[t], (g - 1) & 1);
       tc_fence_after();
+      if constexpr (SPEC) flag_overflow(l, overflow_flag);
       const int row = it.q0 + t * kTcBQ + q4 * 32 + lane;
       store_o<HD>(o_tm, l, out + static_cast<int64_t>(it.s_begin + row) * d_model + it.head * HD, row < it.len);
       tc_fence_before();  // O_t reads complete before the next item's first PV overwrites it
@@ -698,10 +727,11 @@ attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_co
   if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
 }
 
-template <int HD, int BKV, int NQ, bool PERSIST>
+template <int HD, int BKV, int NQ, bool PERSIST, bool SPEC>
 static int launch_attn_cfg(const void* qkv, void* out, const int32_t* cu, int n_seq, int max_s, int heads,
                            float scale, int64_t total_rows, void* workspace, cudaStream_t stream) {
   using C = TcAttnCfg<HD, BKV, NQ>;
+  using Lay = TcPersistLayout<HD, BKV, NQ>;
   const uint64_t ld = 3ull * heads * HD;
   const uint64_t dims[2] = {ld, static_cast<uint64_t>(total_rows)};
   const uint64_t strides[1] = {ld * 2};
@@ -715,28 +745,39 @@ static int launch_attn_cfg(const void* qkv, void* out, const int32_t* cu, int n_
   if (!C::kRem) { tqr = tq; tkvr = tkv; }
   const float scale_log2 = scale * 1.4426950408889634f;
   const int qblocks = (max_s + NQ * kTcBQ - 1) / (NQ * kTcBQ);
+  const int64_t n_items = static_cast<int64_t>(qblocks) * heads * n_seq;
+  if (n_items >= INT32_MAX) return set_error(MMK_ERR_UNSUPPORTED, "attention_tc: too many work items");
+  const int persist_grid = static_cast<int>(n_items < num_sms() ? n_items : num_sms());  // one CTA per SM
   __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out);
-  if constexpr (PERSIST) {
-    using Lay = TcPersistLayout<HD, BKV, NQ>;
-    const int64_t n_items = static_cast<int64_t>(qblocks) * heads * n_seq;
-    if (n_items >= INT32_MAX) return set_error(MMK_ERR_UNSUPPORTED, "attention_tc: too many work items");
-    static std::atomic<uint64_t> attr_done{0};
-    rc = ensure_smem_attr(reinterpret_cast<const void*>(attn_fwd_tc_persistent<HD, BKV, NQ>), Lay::kSmem, attr_done,
-                          "attention_tc: cudaFuncSetAttribute");
+  // workspace: [0] work-item counter of the main pass, [1] overflow flag, [2] counter of the exact redo
+  int* ws = reinterpret_cast<int*>(workspace);
+  cudaError_t me = cudaMemsetAsync(ws, 0, 4 * sizeof(int), stream);
+  if (me != cudaSuccess) return set_cuda_error(me, "attention_tc: workspace reset");
+  if constexpr (PERSIST || SPEC) {
+    static std::atomic<uint64_t> attr_p{0}, attr_x{0};
+    rc = ensure_smem_attr(reinterpret_cast<const void*>(attn_fwd_tc_persistent<HD, BKV, NQ, SPEC>), Lay::kSmem,
+                          attr_p, "attention_tc: cudaFuncSetAttribute");
+    if (!rc && SPEC)
+      rc = ensure_smem_attr(reinterpret_cast<const void*>(attn_fwd_tc_persistent<HD, BKV, NQ, false>), Lay::kSmem,
+                            attr_x, "attention_tc: cudaFuncSetAttribute");
     if (rc) return rc;
-    cudaError_t me = cudaMemsetAsync(workspace, 0, sizeof(int), stream);  // work-item counter
-    if (me != cudaSuccess) return set_cuda_error(me, "attention_tc: workspace reset");
-    const int grid = static_cast<int>(n_items < num_sms() ? n_items : num_sms());  // one CTA per SM
-    attn_fwd_tc_persistent<HD, BKV, NQ><<<grid, C::kThreads, Lay::kSmem, stream>>>(
-        tq, tqr, tkv, tkvr, o, cu, n_seq, heads, qblocks, scale_log2, reinterpret_cast<int*>(workspace));
+  }
+  if constexpr (PERSIST) {
+    attn_fwd_tc_persistent<HD, BKV, NQ, SPEC><<<persist_grid, C::kThreads, Lay::kSmem, stream>>>(
+        tq, tqr, tkv, tkvr, o, cu, n_seq, heads, qblocks, scale_log2, ws, ws + 1, nullptr);
   } else {
     static std::atomic<uint64_t> attr_done{0};
-    rc = ensure_smem_attr(reinterpret_cast<const void*>(attn_fwd_tc<HD, BKV, NQ>), C::kSmem, attr_done,
+    rc = ensure_smem_attr(reinterpret_cast<const void*>(attn_fwd_tc<HD, BKV, NQ, SPEC>), C::kSmem, attr_done,
                           "attention_tc: cudaFuncSetAttribute");
     if (rc) return rc;
     if (n_seq > 65535 || heads > 65535) return set_error(MMK_ERR_UNSUPPORTED, "attention: too many sequences/heads");
-    attn_fwd_tc<HD, BKV, NQ><<<dim3(qblocks, heads, n_seq), C::kThreads, C::kSmem, stream>>>(
-        tq, tqr, tkv, tkvr, o, cu, heads, scale_log2);
+    attn_fwd_tc<HD, BKV, NQ, SPEC><<<dim3(qblocks, heads, n_seq), C::kThreads, C::kSmem, stream>>>(
+        tq, tqr, tkv, tkvr, o, cu, heads, scale_log2, ws + 1);
+  }
+  if constexpr (SPEC) {
+    // exact redo of the whole launch, gated on the overflow flag (all CTAs exit at once when clear)
+    attn_fwd_tc_persistent<HD, BKV, NQ, false><<<persist_grid, C::kThreads, Lay::kSmem, stream>>>(
+        tq, tqr, tkv, tkvr, o, cu, n_seq, heads, qblocks, scale_log2, ws + 2, nullptr, ws + 1);
   }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "attention_tc: launch");
@@ -757,12 +798,19 @@ int launch_attn_tc(const void* qkv, void* out, const int32_t* cu, int n_seq, int
     const char* e = getenv("MMK_ATTN_PERSIST");
     return e ? atoi(e) : -1;
   }();
+  static const bool spec = [] {
+    const char* e = getenv("MMK_ATTN_SPEC");
+    return e ? atoi(e) != 0 : true;
+  }();
   constexpr int BKV = HD == 64 ? 64 : 112, NQ = HD == 64 ? 3 : 2;
   const int64_t items = static_cast<int64_t>((max_s + NQ * kTcBQ - 1) / (NQ * kTcBQ)) * heads * n_seq;
   const bool persist = force == 1 || (force != 0 && HD == 64 && items > 2 * num_sms());
-  if (persist)
-    return launch_attn_cfg<HD, BKV, NQ, true>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, workspace, stream);
-  return launch_attn_cfg<HD, BKV, NQ, false>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, workspace, stream);
+  if (persist) {
+    if (spec) return launch_attn_cfg<HD, BKV, NQ, true, true>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, workspace, stream);
+    return launch_attn_cfg<HD, BKV, NQ, true, false>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, workspace, stream);
+  }
+  if (spec) return launch_attn_cfg<HD, BKV, NQ, false, true>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, workspace, stream);
+  return launch_attn_cfg<HD, BKV, NQ, false, false>(qkv, out, cu, n_seq, max_s, heads, scale, total_rows, workspace, stream);
 }
 
 template int launch_attn_tc<64>(const void*, void*, const int32_t*, int, int, int, float, int64_t, void*, cudaStream_t);

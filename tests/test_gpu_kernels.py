@@ -200,6 +200,32 @@ def test_attention_varlen(mk, hd, heads, lens):
     assert err < 2e-2, err
 
 
+@pytest.mark.parametrize("hd,heads,lens", [(80, 2, [1601, 3202]), (64, 2, [577, 577])])
+@pytest.mark.parametrize("growth", [30.0, 3000.0])
+def test_attention_late_large_scores(mk, hd, heads, lens, growth):
+    """Scores in a late KV tile far above the first tile's: +`growth`/sqrt(hd)*log2(e) in log2 units.
+    30 stays inside the speculative range (P up to ~2^5.. 2^7, no redo); 3000 overflows it (P = inf)
+    and must be recomputed exactly by the gated second pass."""
+    _, ops, _ = mk
+    T = sum(lens)
+    d = heads * hd
+    g = torch.Generator(device="cuda").manual_seed(11)
+    qkv = torch.randn(T, 3 * d, device="cuda", generator=g) * 0.5
+    u = torch.ones(hd, device="cuda") / hd ** 0.5
+    start = 0
+    for L in lens:
+        qkv[start:start + L, 0:hd] += u                                  # head 0 queries lean on u
+        qkv[start + L - 7, d:d + hd] = u * growth                        # one late key, head 0
+        start += L
+    qkv = qkv.bfloat16()
+    cu = torch.tensor(np.concatenate([[0], np.cumsum(lens)]), dtype=torch.int32, device="cuda")
+    out = ops.attention(qkv, cu, len(lens), max(lens), heads, hd)
+    ref = _attn_ref(qkv, lens, heads, hd)
+    assert torch.isfinite(out.float()).all()
+    err = (out.float() - ref).abs().max().item()
+    assert err < 2e-2, err
+
+
 # ----------------------------------------------------------------------------- norms / embed / pack
 def test_layernorm_and_tile_add(mk):
     _, ops, _ = mk
