@@ -200,7 +200,8 @@ def test_attention_varlen(mk, hd, heads, lens):
     assert err < 2e-2, err
 
 
-@pytest.mark.parametrize("hd,heads,lens", [(80, 2, [1601, 3202]), (64, 2, [577, 577])])
+@pytest.mark.parametrize("hd,heads,lens", [(80, 2, [1601, 3202]), (64, 2, [577, 577]),
+                                           (64, 16, [577] * 24)])  # the last runs the persistent kernel
 @pytest.mark.parametrize("growth", [30.0, 3000.0])
 def test_attention_late_large_scores(mk, hd, heads, lens, growth):
     """Scores in a late KV tile far above the first tile's: +`growth`/sqrt(hd)*log2(e) in log2 units.
