@@ -1,8 +1,12 @@
 """Torch-tensor wrappers over the libmmk C ABI (device memory from the PyTorch caching
 allocator, the current CUDA stream, raw pointers across the boundary).  No compute happens in
-Python; every function launches exactly one libmmk kernel (GEMM: one persistent launch)."""
+Python; every function launches one libmmk kernel (GEMM: one persistent launch), except
+attention: the speculative pass plus the exact pass gated on its overflow flag (normally an
+immediate exit)."""
 
 from __future__ import annotations
+
+import os
 
 import torch
 
@@ -31,8 +35,8 @@ class LaunchLog:
         e.record()
         return e
 
-    def end(self, kind, work, start):
-        self.count += 1
+    def end(self, kind, work, start, launches=1):
+        self.count += launches
         if start is not None:
             e = torch.cuda.Event(enable_timing=True)
             e.record()
@@ -59,9 +63,9 @@ def _begin():
     return LOG.begin() if LOG is not None else None
 
 
-def _end(kind, work, start):
+def _end(kind, work, start, launches=1):
     if LOG is not None:
-        LOG.end(kind, work, start)
+        LOG.end(kind, work, start, launches)
 
 
 def _p(t):
@@ -173,6 +177,7 @@ def _attn_flops(cu_seqlens, heads, head_dim):
 
 
 _ATTN_WS_BYTES = int(_lib.lib.mmk_attention_workspace_size())
+_ATTN_LAUNCHES = 1 if os.environ.get("MMK_ATTN_SPEC", "1") == "0" else 2  # speculative + gated exact pass
 
 
 def attention(qkv, cu_seqlens, n_seq: int, max_seqlen: int, heads: int, head_dim: int, out=None,
@@ -187,7 +192,7 @@ def attention(qkv, cu_seqlens, n_seq: int, max_seqlen: int, heads: int, head_dim
     _t0 = _begin()
     _lib.check(_lib.lib.mmk_attention_varlen_bf16(qkv.data_ptr(), out.data_ptr(), cu_seqlens.data_ptr(), n_seq,
                                                   max_seqlen, T, heads, head_dim, float(scale), ws.data_ptr(), _s()))
-    _end('attention', _attn_flops(cu_seqlens, heads, head_dim), _t0)
+    _end('attention', _attn_flops(cu_seqlens, heads, head_dim), _t0, launches=_ATTN_LAUNCHES)
     return out
 
 
