@@ -36,6 +36,7 @@ class ImageBatch:
     dims: list                 # host [(w, h)]
     h2d_bytes: int = 0
     chw: bool = False          # pixel layout of src: HWC (host decoders) or CHW planes (GPU JPEG decode)
+    ready: "torch.cuda.Event | None" = None  # set when staged on a side stream: encode() waits on it
 
     @property
     def n(self) -> int:
@@ -67,7 +68,10 @@ def _as_hwc_u8(img) -> np.ndarray | torch.Tensor:
 
 
 def stage_images(images, device="cuda", pinned: bool = True, stream=None) -> ImageBatch:
-    """Concatenate uint8 HWC images (host arrays or tensors) into one device buffer."""
+    """Concatenate uint8 HWC images (host arrays or tensors) into one device buffer.
+
+    stream: a side CUDA stream for the host-to-device copy, so staging the next batch overlaps
+    the encode of the current one; ``ImagePathExecutor.encode`` waits on the copy's event."""
     imgs = [_as_hwc_u8(i) for i in images]
     dims = [(int(i.shape[1]), int(i.shape[0])) for i in imgs]
     for w, h in dims:
@@ -89,12 +93,20 @@ def stage_images(images, device="cuda", pinned: bool = True, stream=None) -> Ima
     hmeta = torch.from_numpy(meta)
     if pinned:
         hmeta = hmeta.pin_memory()
-    src = host.to(dev, non_blocking=True)
-    dmeta = hmeta.to(dev, non_blocking=True)
+    ready = None
+    if stream is not None:
+        with torch.cuda.stream(stream):
+            src = host.to(dev, non_blocking=True)
+            dmeta = hmeta.to(dev, non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(stream)
+    else:
+        src = host.to(dev, non_blocking=True)
+        dmeta = hmeta.to(dev, non_blocking=True)
     n = len(imgs)
     src_off = dmeta[:2 * n].view(torch.int64)
     return ImageBatch(src=src, src_off=src_off, w=dmeta[2 * n:3 * n], h=dmeta[3 * n:4 * n], dims=dims,
-                      h2d_bytes=total + meta.nbytes)
+                      h2d_bytes=total + meta.nbytes, ready=ready)
 
 
 @dataclass
@@ -170,6 +182,11 @@ class ImagePathExecutor:
         n = batch.n
         if n == 0:
             raise SpecError("encode batch must contain at least one image")
+        if batch.ready is not None:  # staged on a side stream: order after the copy, keep the memory
+            compute = torch.cuda.current_stream(self.device)
+            compute.wait_event(batch.ready)
+            for t in (batch.src, batch.src_off, batch.w, batch.h):
+                t.record_stream(compute)
         tiles = [tile_count(w, h, spec) for w, h in batch.dims]
         total_tiles = sum(tiles)
         P = (spec.tile_edge_px // enc.patch_px) ** 2

@@ -327,3 +327,23 @@ def test_gpu_jpeg_decode_large_batch_chunked(mk):
         ref = decode_jpeg(jpegs[i], device="cuda").reshape(-1)
         w, h = dims[i]
         assert torch.equal(b.src[offs[i]:offs[i] + w * h * 3], ref)
+
+
+def test_stage_images_side_stream_matches(mk):
+    """H2D on a side stream (next batch staged during the current encode) gives identical output."""
+    core, ops, encoders = mk
+    import dataclasses
+    from paper_2502_00937_b200.executor import ImagePathExecutor, stage_images
+    base = core.get_model_spec("llama3.2-11b")
+    spec = dataclasses.replace(base, encoder=dataclasses.replace(base.encoder, layers=1, global_layers=1,
+                                                                 out_layers=(1,)))
+    imgs = _rand_images([(640, 480), (300, 900), (1200, 1200)], 6)
+    ex = ImagePathExecutor(spec, seed=0)
+    ref = ex.encode(stage_images(imgs))
+    side = torch.cuda.Stream()
+    b1 = stage_images(imgs, stream=side)
+    b2 = stage_images(imgs, stream=side)
+    o1 = ex.encode(b1)
+    o2 = ex.encode(b2)
+    torch.cuda.synchronize()
+    assert torch.equal(o1.embeds, ref.embeds) and torch.equal(o2.embeds, ref.embeds)
