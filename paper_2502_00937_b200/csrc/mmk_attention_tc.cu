@@ -404,6 +404,10 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
       const uint32_t p_tm = tmem + C::kPBase + t * C::kPStride;
       const uint32_t q_addr = smem_u32(tile_ptr(C::kQOff + t * C::kQBytes));
       mbar_wait(q_full, 0);
+      // Tile t > 0 starts once tile 0's first P is written: the two softmax warpgroups then run
+      // their exponential phases offset instead of in lockstep, so one warpgroup's S-load / P-store
+      // gaps are filled by the other's MUFU work (attention +2 % in-step, r01_attention.md).
+      if (t > 0 && nkv > 1) mbar_wait(&p_full[0], 0);
       tc_fence_after();
       for (int j = 0; j <= nkv; ++j) {
         const int st = j % C::STAGES;
