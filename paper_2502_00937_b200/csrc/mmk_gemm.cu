@@ -265,10 +265,8 @@ struct Gemm2Smem {
   static constexpr int kBBytes = (kGemm2BN / 2) * kGemmBK * 2;  // this CTA's half of B
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kEpiOffset = STAGES * kStageBytes;
-  // bf16 epilogues: 8 warps x 2 x [32 rows][128 B] staging; residual epilogue: 8 warps x the
-  // warp's whole fp32 residual slice (4 chunks of [32 rows][32 fp32])
   // 8 warps x 2 x [32 rows][128 B]: bf16 output staging, or the residual ring (2 fp32 chunks of
-  // [32 rows][32 cols] per warp)
+  // [32 rows][32 cols] per warp; 3- and 4-slot rings with 4 / 3 mainloop stages measured slower)
   static constexpr int kEpiBytes = 8 * 2 * 4096;
   static constexpr int kBarOffset = kEpiOffset + kEpiBytes;
   static constexpr int kTotal = kBarOffset + 512 + 1024;
