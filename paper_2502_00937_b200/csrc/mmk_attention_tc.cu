@@ -14,9 +14,10 @@
 // Online softmax in base 2 with a lazily updated running max (rescale O only when the row max
 // grows by more than 2^8), so O is rarely touched.
 //
-// Two launch forms share the per-tile steps: one (query block, head, image) work item per CTA
-// (head_dim 80), and a persistent kernel pulling items from a global counter (head_dim 64 with
-// more than two waves of items), see attn_fwd_tc_persistent.
+// Two launch forms share the per-tile steps: a persistent kernel pulling (query block, head,
+// image) work items from a global counter (launches with more than two waves of items), and one
+// item per CTA (smaller launches); see attn_fwd_tc_persistent.  The softmax is speculative (the
+// row max of an item's first KV tile is reused for the rest) with a gated exact pass behind it.
 //
 // head_dim 80 = 64 + 16: Q/K use a 128B-swizzled K-major block (4 MMA k-steps) plus a
 // 32B-swizzled block (1 k-step); V is the MN-major B operand, split into N=64 (128B swizzle)
