@@ -11,8 +11,9 @@
 //   arrangement by Mllama's scale criterion) and the resized image size (integer version of
 //   transformers' get_image_size_fit_to_canvas, or CLIP's shortest-edge resize).
 //
-// One CTA of 1024 threads; thread t owns a contiguous run of images; warp-shuffle scan +
-// shared-memory scan of the 32 warp totals.
+// Two launches: a thread per image for the plan (tile count, canvas, aspect-ratio id), then one
+// CTA scanning the tile counts in coalesced 1024-image chunks (warp-shuffle + shared-memory scan,
+// int64 carry between chunks).
 #include "sm100_common.cuh"
 #include "mmk_internal.h"
 
@@ -89,76 +90,86 @@ __host__ __device__ inline TileGeom plan_one(int64_t w, int64_t h, int64_t T, in
   return g;
 }
 
-constexpr int kPlanThreads = 1024;
+constexpr int kMapThreads = 256;
+constexpr int kScanThreads = 1024;
 
-__global__ void __launch_bounds__(kPlanThreads)
-tile_plan_kernel(const int32_t* __restrict__ w, const int32_t* __restrict__ h, int n, int T, int tok_per_tile,
-                 int cap, int thumb, int mode, int32_t* __restrict__ tiles, int64_t* __restrict__ tile_off,
-                 int64_t* __restrict__ tok_off, int32_t* __restrict__ geom, int32_t* __restrict__ ar_id,
-                 int32_t* __restrict__ bad) {
+// K0a: one thread per image — tile count, canvas geometry, aspect-ratio id (fully parallel).
+__global__ void __launch_bounds__(kMapThreads)
+tile_plan_map_kernel(const int32_t* __restrict__ w, const int32_t* __restrict__ h, int n, int T, int cap, int thumb,
+                     int mode, int32_t* __restrict__ tiles, int32_t* __restrict__ geom, int32_t* __restrict__ ar_id) {
+  const int i = blockIdx.x * kMapThreads + threadIdx.x;
+  if (i >= n) return;
+  const TileGeom g = plan_one(w[i], h[i], T, cap, thumb != 0, mode);
+  tiles[i] = g.tiles;
+  if (geom) {
+    geom[4 * i + 0] = g.rows; geom[4 * i + 1] = g.cols;
+    geom[4 * i + 2] = g.new_w; geom[4 * i + 3] = g.new_h;
+  }
+  if (ar_id) {
+    // index of (rows, cols) in [(a, b) for a in 1..cap for b in 1..cap if a*b <= cap], + 1
+    int id = 0;
+    if (g.tiles > 0) {
+      id = g.cols;
+      for (int a = 1; a < g.rows; ++a) id += cap / a;
+    }
+    ar_id[i] = id;
+  }
+}
+
+// K0b: one CTA, coalesced 1024-image chunks: exclusive int64 prefix sums of the tile counts
+// (Request.total_tiles / total_image_tokens offsets) and the count of rejected images.
+__global__ void __launch_bounds__(kScanThreads)
+tile_plan_scan_kernel(const int32_t* __restrict__ tiles, int n, int tok_per_tile, int64_t* __restrict__ tile_off,
+                      int64_t* __restrict__ tok_off, int32_t* __restrict__ bad) {
   __shared__ int64_t warp_tot[32];
   __shared__ int32_t warp_bad[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int per = (n + kPlanThreads - 1) / kPlanThreads;
-  const int i0 = tid * per;
-  const int i1 = min(n, i0 + per);
-  int64_t local = 0;
+  int64_t carry = 0;
   int32_t nbad = 0;
-  for (int i = i0; i < i1; ++i) {
-    const TileGeom g = plan_one(w[i], h[i], T, cap, thumb != 0, mode);
-    tiles[i] = g.tiles;
-    if (geom) {
-      geom[4 * i + 0] = g.rows; geom[4 * i + 1] = g.cols;
-      geom[4 * i + 2] = g.new_w; geom[4 * i + 3] = g.new_h;
-    }
-    if (ar_id) {
-      // index of (rows, cols) in [(a, b) for a in 1..cap for b in 1..cap if a*b <= cap], + 1
-      int id = 0;
-      if (g.tiles > 0) {
-        id = g.cols;
-        for (int a = 1; a < g.rows; ++a) id += cap / a;
-      }
-      ar_id[i] = id;
-    }
-    nbad += (g.tiles == 0);
-    local += g.tiles;
-  }
-  // inclusive warp scan
-  int64_t incl = local;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  int32_t wb = nbad;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) wb += __shfl_xor_sync(0xffffffffu, wb, o);
-  if (lane == 31) warp_tot[warp] = incl;
-  if (lane == 0) warp_bad[warp] = wb;
-  __syncthreads();
-  if (warp == 0) {
-    int64_t t = warp_tot[lane];
-    int64_t s = t;
+  for (int base = 0; base < n; base += kScanThreads) {
+    const int i = base + tid;
+    const int64_t v = i < n ? tiles[i] : 0;
+    nbad += (i < n && v == 0);
+    int64_t incl = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int64_t v = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += v;
+      const int64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
     }
-    warp_tot[lane] = s - t;  // exclusive warp offsets
-    int32_t b = warp_bad[lane];
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const int64_t t = warp_tot[lane];
+      int64_t x = t;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
-    if (lane == 0 && bad) *bad = b;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t u = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += u;
+      }
+      warp_tot[lane] = x - t;  // exclusive offsets of the warps
+    }
+    __syncthreads();
+    const int64_t excl = carry + warp_tot[warp] + incl - v;
+    if (i < n) {
+      tile_off[i] = excl;
+      tok_off[i] = excl * tok_per_tile;
+    }
+    __syncthreads();
+    if (tid == kScanThreads - 1) warp_tot[0] = excl + v - carry;  // this chunk's total
+    __syncthreads();
+    carry += warp_tot[0];
+    __syncthreads();
   }
+  for (int o = 16; o > 0; o >>= 1) nbad += __shfl_xor_sync(0xffffffffu, nbad, o);
+  if (lane == 0) warp_bad[warp] = nbad;
   __syncthreads();
-  int64_t run = warp_tot[warp] + incl - local;  // exclusive prefix of this thread's first image
-  for (int i = i0; i < i1; ++i) {
-    tile_off[i] = run;
-    tok_off[i] = run * tok_per_tile;
-    run += tiles[i];
+  if (tid == 0) {
+    int32_t b = 0;
+    for (int k = 0; k < kScanThreads / 32; ++k) b += warp_bad[k];
+    if (bad) *bad = b;
+    tile_off[n] = carry;
+    tok_off[n] = carry * tok_per_tile;
   }
-  if (i1 == n && i0 < n) { tile_off[n] = run; tok_off[n] = run * tok_per_tile; }
-  if (n == 0 && tid == 0) { tile_off[0] = 0; tok_off[0] = 0; }
 }
 
 // Per-tile (image index, slot within image) for the embedding / tile-position kernels.
@@ -185,8 +196,10 @@ extern "C" int mmk_tile_plan(const int32_t* w, const int32_t* h, int32_t n, int3
   if (tile_px < 1 || tokens_per_tile < 1 || max_tiles < 1)
     return set_error(MMK_ERR_ARG, "tile_plan: tile_edge_px, tokens_per_tile, max_tiles must be >= 1");
   if (resize_mode != 0 && resize_mode != 1) return set_error(MMK_ERR_ARG, "tile_plan: resize_mode must be 0 or 1");
-  tile_plan_kernel<<<1, kPlanThreads, 0, stream>>>(w, h, n, tile_px, tokens_per_tile, max_tiles, thumbnail,
-                                                   resize_mode, tiles, tile_off, tok_off, geom, ar_id, bad);
+  if (n > 0)
+    tile_plan_map_kernel<<<(n + kMapThreads - 1) / kMapThreads, kMapThreads, 0, stream>>>(
+        w, h, n, tile_px, max_tiles, thumbnail, resize_mode, tiles, geom, ar_id);
+  tile_plan_scan_kernel<<<1, kScanThreads, 0, stream>>>(tiles, n, tokens_per_tile, tile_off, tok_off, bad);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "tile_plan: launch");
 }
