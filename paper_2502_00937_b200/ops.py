@@ -1,8 +1,8 @@
 """Torch-tensor wrappers over the libmmk C ABI (device memory from the PyTorch caching
 allocator, the current CUDA stream, raw pointers across the boundary).  No compute happens in
-Python; every function launches one libmmk kernel (GEMM: one persistent launch), except
-attention: the speculative pass plus the exact pass gated on its overflow flag (normally an
-immediate exit)."""
+Python; every function launches one libmmk kernel (GEMM: one persistent launch), except the
+tile plan (per-image kernel + scan) and attention (the speculative pass plus the exact pass
+gated on its overflow flag, normally an immediate exit)."""
 
 from __future__ import annotations
 
@@ -102,7 +102,7 @@ def tile_plan(w: torch.Tensor, h: torch.Tensor, spec, resize_mode: int | None = 
                                       spec.max_tiles_per_image, int(spec.thumbnail_tile), resize_mode,
                                       tiles.data_ptr(), tile_off.data_ptr(), tok_off.data_ptr(), geom.data_ptr(),
                                       ar_id.data_ptr(), bad.data_ptr(), _s()))
-    _end('tile_plan', 0, _t0)
+    _end('tile_plan', 0, _t0, launches=2 if n > 0 else 1)  # per-image plan + scan
     return {"tiles": tiles, "tile_off": tile_off, "tok_off": tok_off, "geom": geom, "ar_id": ar_id, "bad": bad}
 
 
