@@ -1,5 +1,6 @@
 // mmk_api.cu — error reporting, device queries and TMA descriptor encoding for libmmk.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -20,6 +21,14 @@ int set_error(int code, const char* fmt, ...) {
 int set_cuda_error(cudaError_t e, const char* where) {
   snprintf(g_err, sizeof(g_err), "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
   return MMK_ERR_CUDA;
+}
+
+bool pdl_for(bool small) {
+  static const int mode = [] {  // -1 auto (small launches only), 0 off, 1 every launch
+    const char* e = getenv("MMK_PDL");
+    return e == nullptr ? -1 : atoi(e) != 0;
+  }();
+  return mode == 1 || (mode == -1 && small);
 }
 
 int num_sms() {

@@ -326,6 +326,7 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
   uint64_t* pv_done = p_full + NQ;             // [NQ] MMA -> softmax: PV_t retired
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + NQ);
 
+  griddep_wait();  // cu_seqlens / QKV come from the preceding kernels (PDL)
   const int head = blockIdx.y, seq = blockIdx.z;  // heads of one image adjacent: K/V lines shared in L2
   const int s_begin = cu_seqlens[seq];
   const int len = cu_seqlens[seq + 1] - s_begin;
@@ -365,6 +366,7 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  griddep_launch_dependents();
 
   auto tile_ptr = [&](int off) { return smem + off; };
 
@@ -506,7 +508,10 @@ attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_co
                        __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ cu_seqlens, int n_seq,
                        int heads, int qblocks, float scale_log2, int* __restrict__ item_counter,
                        int* __restrict__ overflow_flag, const int* __restrict__ gate) {
-  if (gate != nullptr && *reinterpret_cast<const volatile int*>(gate) == 0) return;
+  if (gate != nullptr) {  // the flag is written by the speculative pass just before (PDL)
+    griddep_wait();
+    if (*reinterpret_cast<const volatile int*>(gate) == 0) return;
+  }
   using C = TcAttnCfg<HD, BKV, NQ>;
   using Lay = TcPersistLayout<HD, BKV, NQ>;
   constexpr int kTmaWarp = 4 * NQ, kMmaWarp = 4 * NQ + 1;  // MMA warp of query tile t: kMmaWarp + t
@@ -567,6 +572,8 @@ attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_co
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  griddep_wait();  // setup above overlaps the previous kernel's tail (PDL)
+  griddep_launch_dependents();
   auto tile_ptr = [&](int off) { return smem + off; };
   // consumer side of the ring: copy item k, release its slot
   auto next_item = [&](uint32_t& k) -> AttnItem {
@@ -770,21 +777,26 @@ static int launch_attn_cfg(const void* qkv, void* out, const int32_t* cu, int n_
     if (rc) return rc;
   }
   if constexpr (PERSIST) {
-    attn_fwd_tc_persistent<HD, BKV, NQ, SPEC><<<persist_grid, C::kThreads, Lay::kSmem, stream>>>(
-        tq, tqr, tkv, tkvr, o, cu, n_seq, heads, qblocks, scale_log2, ws, ws + 1, nullptr);
+    me = launch_kernel(attn_fwd_tc_persistent<HD, BKV, NQ, SPEC>, dim3(persist_grid), dim3(C::kThreads), Lay::kSmem,
+                       stream, 1, false, tq, tqr, tkv, tkvr, o, cu, n_seq, heads, qblocks, scale_log2, ws, ws + 1,
+                       static_cast<const int*>(nullptr));
+    if (me != cudaSuccess) return set_cuda_error(me, "attention_tc: launch");
   } else {
     static std::atomic<uint64_t> attr_done{0};
     rc = ensure_smem_attr(reinterpret_cast<const void*>(attn_fwd_tc<HD, BKV, NQ, SPEC>), C::kSmem, attr_done,
                           "attention_tc: cudaFuncSetAttribute");
     if (rc) return rc;
     if (n_seq > 65535 || heads > 65535) return set_error(MMK_ERR_UNSUPPORTED, "attention: too many sequences/heads");
-    attn_fwd_tc<HD, BKV, NQ, SPEC><<<dim3(qblocks, heads, n_seq), C::kThreads, C::kSmem, stream>>>(
-        tq, tqr, tkv, tkvr, o, cu, heads, scale_log2, ws + 1);
+    me = launch_kernel(attn_fwd_tc<HD, BKV, NQ, SPEC>, dim3(qblocks, heads, n_seq), dim3(C::kThreads), C::kSmem,
+                       stream, 1, true, tq, tqr, tkv, tkvr, o, cu, heads, scale_log2, ws + 1);
+    if (me != cudaSuccess) return set_cuda_error(me, "attention_tc: launch");
   }
   if constexpr (SPEC) {
     // exact redo of the whole launch, gated on the overflow flag (all CTAs exit at once when clear)
-    attn_fwd_tc_persistent<HD, BKV, NQ, false><<<persist_grid, C::kThreads, Lay::kSmem, stream>>>(
-        tq, tqr, tkv, tkvr, o, cu, n_seq, heads, qblocks, scale_log2, ws + 2, nullptr, ws + 1);
+    me = launch_kernel(attn_fwd_tc_persistent<HD, BKV, NQ, false>, dim3(persist_grid), dim3(C::kThreads),
+                       Lay::kSmem, stream, 1, !PERSIST, tq, tqr, tkv, tkvr, o, cu, n_seq, heads, qblocks, scale_log2, ws + 2,
+                       static_cast<int*>(nullptr), static_cast<const int*>(ws + 1));
+    if (me != cudaSuccess) return set_cuda_error(me, "attention_tc: launch");
   }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "attention_tc: launch");

@@ -157,6 +157,8 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();  // setup above overlaps the previous kernel's tail (PDL)
+  griddep_launch_dependents();
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (warp-uniform)
@@ -356,6 +358,8 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();  // setup above overlaps the previous kernel's tail (PDL)
+  griddep_launch_dependents();
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer (both CTAs)
@@ -570,8 +574,8 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int 
     return rc;
   const int tiles = ((M + kGemmBM - 1) / kGemmBM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, kGemmThreads, S::kTotal, stream>>>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_kernel(kern, dim3(grid), dim3(kGemmThreads), S::kTotal, stream, 1, tiles <= 2 * num_sms(), ta, tb, M, N, K, bias,
+                                out, ldo, gate, aux, ld_aux);
   if (e != cudaSuccess) return set_cuda_error(e, "gemm: launch");
   return MMK_OK;
 }
@@ -604,19 +608,8 @@ static int launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, const C
   const int tiles = ((M + 255) / 256) * (N / kGemm2BN);
   const int pairs_max = num_sms() / 2;
   const int pairs = tiles < pairs_max ? tiles : pairs_max;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2 * pairs);
-  cfg.blockDim = dim3(kGemmThreads);
-  cfg.dynamicSmemBytes = S::kTotal;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux);
+  cudaError_t e = launch_kernel(kern, dim3(2 * pairs), dim3(kGemmThreads), S::kTotal, stream, 2, tiles <= num_sms(), ta, tb, to, M, N, K,
+                                bias, out, ldo, gate, aux, ld_aux);
   if (e != cudaSuccess) return set_cuda_error(e, "gemm2: launch");
   return MMK_OK;
 }

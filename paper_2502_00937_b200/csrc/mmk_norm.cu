@@ -64,6 +64,8 @@ layernorm_kernel(const float* __restrict__ x, void* y, int y_f32, int rows, int 
                  const float* __restrict__ beta, float eps, const float* __restrict__ tile_add,
                  const int32_t* __restrict__ tile_image, const int32_t* __restrict__ image_table,
                  const int32_t* __restrict__ tile_slot, int rows_per_tile, int slots) {
+  griddep_wait();  // PDL: inputs come from the preceding kernel
+  griddep_launch_dependents();
   const int lane = threadIdx.x & 31;
   const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -91,6 +93,8 @@ embed_kernel(const float* __restrict__ patch_out, const int32_t* __restrict__ ti
              const float* __restrict__ tile_pos, float tile_pos_scale, const float* __restrict__ pre_tile,
              float pre_scale, int slots, const float* __restrict__ gamma, const float* __restrict__ beta, float eps,
              float* __restrict__ resid) {
+  griddep_wait();  // PDL: inputs come from the preceding kernel
+  griddep_launch_dependents();
   const int lane = threadIdx.x & 31;
   const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   const int64_t rows = static_cast<int64_t>(total_tiles) * (P + 1);
@@ -132,6 +136,8 @@ embed_kernel(const float* __restrict__ patch_out, const int32_t* __restrict__ ti
 __global__ void __launch_bounds__(128)
 pack_mllama_kernel(const float* __restrict__ fin, const __nv_bfloat16* __restrict__ inter, int n_inter, int rows,
                    int d, __nv_bfloat16* __restrict__ out) {
+  griddep_wait();  // PDL: inputs come from the preceding kernel
+  griddep_launch_dependents();
   extern __shared__ __align__(16) __nv_bfloat16 s_inter[];  // [n_inter][d]
   const int64_t row = blockIdx.x;
   const int64_t ldo = static_cast<int64_t>(d) * (1 + n_inter);
@@ -163,6 +169,8 @@ pack_mllama_kernel(const float* __restrict__ fin, const __nv_bfloat16* __restric
 __global__ void __launch_bounds__(256)
 pack_drop_kernel(const void* __restrict__ src, int src_f32, int64_t out_rows, int tokens_per_tile, int drop, int d,
                  __nv_bfloat16* __restrict__ out) {
+  griddep_wait();  // PDL: inputs come from the preceding kernel
+  griddep_launch_dependents();
   const int keep = tokens_per_tile - drop;
   const int64_t orow = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   if (orow >= out_rows) return;
@@ -184,6 +192,8 @@ pack_drop_kernel(const void* __restrict__ src, int src_f32, int64_t out_rows, in
 }
 
 __global__ void checksum_kernel(const __nv_bfloat16* __restrict__ x, int64_t n, float* out) {
+  griddep_wait();  // PDL: inputs come from the preceding kernel
+  griddep_launch_dependents();
   float s = 0.f;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -201,7 +211,7 @@ using namespace mmk;
 
 #define MMK_LN_CASE(V)                                                                                       \
   case V:                                                                                                    \
-    layernorm_kernel<V><<<grid_rows(rows), 256, 0, stream>>>(x, y, y_f32, rows, d, gamma, beta, eps, tile_add, \
+    (void)launch_kernel(layernorm_kernel<V>, dim3(grid_rows(rows)), dim3(256), 0, stream, 1, rows <= kSmallRows, x, y, y_f32, rows, d, gamma, beta, eps, tile_add, \
                                                              tile_image, image_table, tile_slot, rows_per_tile, \
                                                              slots);                                            \
     break;
@@ -229,7 +239,7 @@ extern "C" int mmk_layernorm(const float* x, void* y, int32_t y_f32, int32_t row
 
 #define MMK_EMB_CASE(V)                                                                                   \
   case V:                                                                                                 \
-    embed_kernel<V><<<grid_rows(rows), 256, 0, stream>>>(patch_out, tile_image, tile_slot, image_ar,      \
+    (void)launch_kernel(embed_kernel<V>, dim3(grid_rows(rows)), dim3(256), 0, stream, 1, rows <= kSmallRows, patch_out, tile_image, tile_slot, image_ar,      \
                                                          total_tiles, patches_per_tile, d, cls, pos,       \
                                                          pos_scale, tile_pos, tile_pos_scale, pre_tile,    \
                                                          pre_scale, slots, gamma, beta, eps, resid);       \
@@ -268,7 +278,7 @@ extern "C" int mmk_pack_mllama(const float* final_resid, const void* inter, int3
     cudaError_t e = cudaFuncSetAttribute(pack_mllama_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return set_cuda_error(e, "pack_mllama: smem attr");
   }
-  pack_mllama_kernel<<<rows, 128, smem, stream>>>(final_resid, reinterpret_cast<const __nv_bfloat16*>(inter), n_inter,
+  (void)launch_kernel(pack_mllama_kernel, dim3(rows), dim3(128), smem, stream, 1, rows <= kSmallRows, final_resid, reinterpret_cast<const __nv_bfloat16*>(inter), n_inter,
                                                   rows, d, reinterpret_cast<__nv_bfloat16*>(out));
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "pack_mllama: launch");
@@ -279,7 +289,7 @@ extern "C" int mmk_pack_drop_cls(const void* src, int32_t src_f32, int32_t tiles
   if (tiles < 0 || tokens_per_tile <= drop || drop < 0 || d % 8 != 0) return set_error(MMK_ERR_ARG, "pack_drop: bad shape");
   const int64_t out_rows = static_cast<int64_t>(tiles) * (tokens_per_tile - drop);
   if (out_rows == 0) return MMK_OK;
-  pack_drop_kernel<<<grid_rows(out_rows), 256, 0, stream>>>(src, src_f32, out_rows, tokens_per_tile, drop, d,
+  (void)launch_kernel(pack_drop_kernel, dim3(grid_rows(out_rows)), dim3(256), 0, stream, 1, out_rows <= kSmallRows, src, src_f32, out_rows, tokens_per_tile, drop, d,
                                                             reinterpret_cast<__nv_bfloat16*>(out));
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "pack_drop: launch");
@@ -290,7 +300,7 @@ extern "C" int mmk_checksum_bf16(const void* x, int64_t n, float* out, cudaStrea
   cudaError_t e = cudaMemsetAsync(out, 0, sizeof(float), stream);
   if (e != cudaSuccess) return set_cuda_error(e, "checksum: memset");
   if (n == 0) return MMK_OK;
-  checksum_kernel<<<4 * num_sms(), 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(x), n, out);
+  (void)launch_kernel(checksum_kernel, dim3(4 * num_sms()), dim3(256), 0, stream, 1, n <= 1024 * kSmallRows, reinterpret_cast<const __nv_bfloat16*>(x), n, out);
   e = cudaGetLastError();
   return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "checksum: launch");
 }

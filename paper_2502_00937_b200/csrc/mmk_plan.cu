@@ -97,6 +97,8 @@ constexpr int kScanThreads = 1024;
 __global__ void __launch_bounds__(kMapThreads)
 tile_plan_map_kernel(const int32_t* __restrict__ w, const int32_t* __restrict__ h, int n, int T, int cap, int thumb,
                      int mode, int32_t* __restrict__ tiles, int32_t* __restrict__ geom, int32_t* __restrict__ ar_id) {
+  griddep_wait();  // PDL: inputs come from the preceding kernel
+  griddep_launch_dependents();
   const int i = blockIdx.x * kMapThreads + threadIdx.x;
   if (i >= n) return;
   const TileGeom g = plan_one(w[i], h[i], T, cap, thumb != 0, mode);
@@ -121,6 +123,8 @@ tile_plan_map_kernel(const int32_t* __restrict__ w, const int32_t* __restrict__ 
 __global__ void __launch_bounds__(kScanThreads)
 tile_plan_scan_kernel(const int32_t* __restrict__ tiles, int n, int tok_per_tile, int64_t* __restrict__ tile_off,
                       int64_t* __restrict__ tok_off, int32_t* __restrict__ bad) {
+  griddep_wait();  // PDL: inputs come from the preceding kernel
+  griddep_launch_dependents();
   __shared__ int64_t warp_tot[32];
   __shared__ int32_t warp_bad[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -175,6 +179,8 @@ tile_plan_scan_kernel(const int32_t* __restrict__ tiles, int n, int tok_per_tile
 // Per-tile (image index, slot within image) for the embedding / tile-position kernels.
 __global__ void tile_index_kernel(const int64_t* __restrict__ tile_off, int n, int32_t* __restrict__ tile_image,
                                   int32_t* __restrict__ tile_slot) {
+  griddep_wait();  // PDL: inputs come from the preceding kernel
+  griddep_launch_dependents();
   const int i = blockIdx.x * blockDim.y + threadIdx.y;
   if (i >= n) return;
   const int64_t a = tile_off[i], b = tile_off[i + 1];
@@ -197,9 +203,9 @@ extern "C" int mmk_tile_plan(const int32_t* w, const int32_t* h, int32_t n, int3
     return set_error(MMK_ERR_ARG, "tile_plan: tile_edge_px, tokens_per_tile, max_tiles must be >= 1");
   if (resize_mode != 0 && resize_mode != 1) return set_error(MMK_ERR_ARG, "tile_plan: resize_mode must be 0 or 1");
   if (n > 0)
-    tile_plan_map_kernel<<<(n + kMapThreads - 1) / kMapThreads, kMapThreads, 0, stream>>>(
+    (void)launch_kernel(tile_plan_map_kernel, dim3((n + kMapThreads - 1) / kMapThreads), dim3(kMapThreads), 0, stream, 1, n <= 4096, 
         w, h, n, tile_px, max_tiles, thumbnail, resize_mode, tiles, geom, ar_id);
-  tile_plan_scan_kernel<<<1, kScanThreads, 0, stream>>>(tiles, n, tokens_per_tile, tile_off, tok_off, bad);
+  (void)launch_kernel(tile_plan_scan_kernel, dim3(1), dim3(kScanThreads), 0, stream, 1, n <= 4096, tiles, n, tokens_per_tile, tile_off, tok_off, bad);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "tile_plan: launch");
 }
@@ -209,7 +215,7 @@ extern "C" int mmk_tile_index(const int64_t* tile_off, int32_t n, int32_t* tile_
   if (n < 0) return set_error(MMK_ERR_ARG, "tile_index: n < 0");
   if (n == 0) return MMK_OK;
   dim3 block(32, 8);
-  tile_index_kernel<<<(n + 7) / 8, block, 0, stream>>>(tile_off, n, tile_image, tile_slot);
+  (void)launch_kernel(tile_index_kernel, dim3((n + 7) / 8), dim3(block), 0, stream, 1, n <= 4096, tile_off, n, tile_image, tile_slot);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "tile_index: launch");
 }

@@ -52,6 +52,8 @@ preprocess_kernel(const uint8_t* __restrict__ src, const int64_t* __restrict__ s
                   const int32_t* __restrict__ geom, int n, int T, int p, int k_pad, int mode, int thumb,
                   const float* __restrict__ scale3, const float* __restrict__ shift3,
                   __nv_bfloat16* __restrict__ patches) {
+  griddep_wait();  // PDL: inputs come from the preceding kernel
+  griddep_launch_dependents();
   __shared__ PrepImage meta;
   __shared__ float s_scale[3], s_shift[3];
   const int per_side = T / p;
@@ -146,11 +148,11 @@ extern "C" int mmk_preprocess(const uint8_t* src, const int64_t* src_off, int32_
   if (n == 0 || total_tiles == 0) return MMK_OK;
   const int blocks = total_tiles * (tile_px / patch_px);
   if (src_chw)
-    preprocess_kernel<true><<<blocks, 256, 0, stream>>>(src, src_off, w, h, tile_off, geom, n, tile_px, patch_px, k_pad,
+    (void)launch_kernel(preprocess_kernel<true>, dim3(blocks), dim3(256), 0, stream, 1, total_tiles <= 64, src, src_off, w, h, tile_off, geom, n, tile_px, patch_px, k_pad,
                                                         mode, thumbnail, scale3, shift3,
                                                         reinterpret_cast<__nv_bfloat16*>(patches));
   else
-    preprocess_kernel<false><<<blocks, 256, 0, stream>>>(src, src_off, w, h, tile_off, geom, n, tile_px, patch_px,
+    (void)launch_kernel(preprocess_kernel<false>, dim3(blocks), dim3(256), 0, stream, 1, total_tiles <= 64, src, src_off, w, h, tile_off, geom, n, tile_px, patch_px,
                                                          k_pad, mode, thumbnail, scale3, shift3,
                                                          reinterpret_cast<__nv_bfloat16*>(patches));
   cudaError_t e = cudaGetLastError();

@@ -158,6 +158,12 @@ MMK_DEV void tmem_dealloc(uint32_t taddr) {  // whole warp
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols)
                : "memory");
 }
+// Programmatic dependent launch: wait until the preceding kernel in the stream has completed and
+// its memory is visible (a no-op when this kernel was launched without the PDL attribute), and
+// let the next kernel's CTAs launch (their prologue then overlaps this kernel's tail).
+MMK_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+MMK_DEV void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 MMK_DEV void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
