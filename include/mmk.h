@@ -90,7 +90,7 @@ int mmk_preprocess(const uint8_t* src, const int64_t* src_off, int32_t src_chw, 
 /*
  * K2/K4/K6/K7/K8 — D[M,N] = A[M,K] . B[N,K]^T on tcgen05 tensor cores (bf16 in, fp32 acc),
  * with the fused epilogue `epilogue` (enum mmk_epilogue).  lda/ldb/ldo/ld_aux in elements.
- * bias: f32 [N] or NULL.  gate: residual scale (RESID_F32 only).  aux: optional bf16 copy of
+ * bias: f32 [N] (16-byte aligned) or NULL.  gate: residual scale (RESID_F32 only).  aux: optional bf16 copy of
  * the updated residual (intermediate-layer capture for K9), RESID_F32 only.
  */
 int mmk_gemm_bf16(const void* a, int64_t lda, const void* b, int64_t ldb, int32_t m, int32_t n,

@@ -62,6 +62,34 @@ MMK_DEV float quick_gelu(float x) {
   return x * r;
 }
 
+// Paired forms (FFMA2 / FMUL2 on the FMA pipe, half the issue slots; same math as above).
+MMK_DEV float2 gelu_erf2(float2 x) {
+  const float2 z = __fmul2_rn(make_float2(fabsf(x.x), fabsf(x.y)), make_float2(0.70710678118654752f, 0.70710678118654752f));
+  const float2 den = __ffma2_rn(make_float2(0.3275911f, 0.3275911f), z, make_float2(1.0f, 1.0f));
+  float2 t;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.x) : "f"(den.x));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.y) : "f"(den.y));
+  float2 p = __ffma2_rn(make_float2(1.061405429f, 1.061405429f), t, make_float2(-1.453152027f, -1.453152027f));
+  p = __ffma2_rn(p, t, make_float2(1.421413741f, 1.421413741f));
+  p = __ffma2_rn(p, t, make_float2(-0.284496736f, -0.284496736f));
+  p = __ffma2_rn(p, t, make_float2(0.254829592f, 0.254829592f));
+  p = __fmul2_rn(p, t);
+  const float2 arg = __fmul2_rn(__fmul2_rn(z, z), make_float2(-1.4426950408889634f, -1.4426950408889634f));
+  float2 e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(arg.x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(arg.y));
+  const float2 erf_abs = __ffma2_rn(make_float2(-p.x, -p.y), e, make_float2(1.0f, 1.0f));
+  const float2 one_p = make_float2(1.0f + copysignf(erf_abs.x, x.x), 1.0f + copysignf(erf_abs.y, x.y));
+  return __fmul2_rn(__fmul2_rn(make_float2(0.5f, 0.5f), x), one_p);
+}
+
+template <int EPI>
+MMK_DEV float2 apply_act2(float2 v) {
+  if constexpr (EPI == MMK_EPI_BF16_GELU) return gelu_erf2(v);
+  else if constexpr (EPI == MMK_EPI_BF16_QUICKGELU) return make_float2(quick_gelu(v.x), quick_gelu(v.y));
+  else return v;
+}
+
 template <int EPI>
 MMK_DEV float apply_act(float v) {
   if constexpr (EPI == MMK_EPI_BF16_GELU) return gelu_erf(v);
@@ -285,13 +313,18 @@ MMK_DEV void epilogue_bf16_tma(const uint32_t (&r0)[32], const uint32_t (&r1)[32
   for (int h = 0; h < 2; ++h) {
     const uint32_t (&r)[32] = h ? r1 : r0;
 #pragma unroll
-    for (int i = 0; i < 32; i += 2) {
-      float a = __uint_as_float(r[i]), b = __uint_as_float(r[i + 1]);
-      if (bias != nullptr) {
-        a += __ldg(bias + col + 32 * h + i);
-        b += __ldg(bias + col + 32 * h + i + 1);
+    for (int i = 0; i < 32; i += 4) {
+      float2 a = make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1]));
+      float2 b = make_float2(__uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+      if (bias != nullptr) {  // one 16-byte broadcast load per 4 columns
+        const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + col + 32 * h + i));
+        a = __fadd2_rn(a, make_float2(b4.x, b4.y));
+        b = __fadd2_rn(b, make_float2(b4.z, b4.w));
       }
-      w[16 * h + i / 2] = pack_bf16x2(apply_act<EPI>(a), apply_act<EPI>(b));
+      a = apply_act2<EPI>(a);
+      b = apply_act2<EPI>(b);
+      w[16 * h + i / 2] = pack_bf16x2(a.x, a.y);
+      w[16 * h + i / 2 + 1] = pack_bf16x2(b.x, b.y);
     }
   }
   if (lane == 0) tma_store_wait_read<1>();  // this buffer's previous store has been read out
@@ -642,8 +675,9 @@ extern "C" int mmk_gemm_bf16(const void* a, int64_t lda, const void* b, int64_t 
   if (n % 32 != 0) return set_error(MMK_ERR_UNSUPPORTED, "gemm: N=%d must be a multiple of 32", n);
   if (lda % 8 != 0 || ldb % 8 != 0 || lda < k || ldb < k)
     return set_error(MMK_ERR_ARG, "gemm: lda/ldb must be >= K and multiples of 8 elements");
-  if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(out)) & 15)
-    return set_error(MMK_ERR_ARG, "gemm: pointers must be 16-byte aligned");
+  if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(out) |
+       reinterpret_cast<uintptr_t>(bias)) & 15)
+    return set_error(MMK_ERR_ARG, "gemm: pointers (a, b, out, bias) must be 16-byte aligned");
   const bool f32_out = epilogue == MMK_EPI_F32 || epilogue == MMK_EPI_RESID_F32;
   if (ldo % (f32_out ? 4 : 8) != 0) return set_error(MMK_ERR_ARG, "gemm: ldo misaligned");
   if (aux != nullptr && (epilogue != MMK_EPI_RESID_F32 || ld_aux % 8 != 0))
