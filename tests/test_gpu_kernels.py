@@ -20,6 +20,7 @@ from oracle import preprocess as oprep  # noqa: E402
 from oracle import tiling as otiling  # noqa: E402
 
 GOLD = Path(__file__).resolve().parent / "golden"
+ROOT = Path(__file__).resolve().parent.parent
 
 
 @pytest.fixture(scope="module")
@@ -349,3 +350,17 @@ def test_stage_images_side_stream_matches(mk):
     o2 = ex.encode(b2)
     torch.cuda.synchronize()
     assert torch.equal(o1.embeds, ref.embeds) and torch.equal(o2.embeds, ref.embeds)
+
+
+def test_plain_c_client_of_the_abi(mk):
+    """examples/c_abi_demo.c: a C program (no Python/PyTorch) drives K0 + K1 through include/mmk.h."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    ex = ROOT / "examples"
+    subprocess.run(["make", "-C", str(ex), "-s"], check=True)
+    r = subprocess.run([str(ex / "c_abi_demo")], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    assert "tok_off 0 3202 8005" in r.stdout  # reference tile_count: 1000x500 -> 2, 560x1200 -> 3
+    assert "bad-arg status ok" in r.stdout
