@@ -47,3 +47,15 @@ def test_argument_errors_map_to_reference_exceptions():
     rc = _lib.lib.mmk_gemm_bf16(None, 64, None, 64, 128, 100, 64, 0, None, None, 100, 1.0, None, 0, None)
     with pytest.raises(_lib.ProfileError):
         _lib.check(rc)
+
+
+def test_header_is_plain_c_and_links():
+    """include/mmk.h compiles as C11 and a C client links against libmmk.so (no GPU needed)."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None or not LIB.exists():
+        pytest.skip("gcc or libmmk.so missing")
+    ex = Path(__file__).resolve().parent.parent / "examples"
+    r = subprocess.run(["make", "-C", str(ex), "-s", "-B"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    (ex / "c_abi_demo").unlink()
