@@ -80,6 +80,14 @@ MMK_DEV float fast_exp2(float x) {
 
 MMK_DEV bool warp_any(bool p) { return __any_sync(0xffffffffu, p); }
 
+// Register dependency fence: values written by an asynchronous tcgen05.ld are only read after
+// the tcgen05.wait::ld that precedes this (the compiler may not hoist their uses above it).
+template <int N>
+MMK_DEV void reg_fence(uint32_t* r) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) asm volatile("" : "+r"(r[i]));
+}
+
 MMK_DEV float fmax3(float a, float b, float c) {
   float d;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
@@ -165,8 +173,21 @@ MMK_DEV void softmax_tile(uint32_t s_tm, uint32_t o_tm, uint32_t p_tm, uint64_t*
   if (trace) { TR(t, j, 1) }
   tc_fence_after();
   uint32_t r[BKV];
+  // Speculative non-first, non-last tiles need no row max, so the exponentials of the first 32
+  // keys start while the other 80 are still in flight from TMEM (S is released after them).
+  const bool pipelined = SPEC && !first && valid >= BKV;  // warp-uniform
+  auto release_s = [&]() {
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(s_free);  // TMEM S_t may now be overwritten by the next S_t
+  };
+  tmem_ld_32x32b_x32(s_tm, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+  if (pipelined) {
+    tmem_ld_wait();
+    reg_fence<32>(r);
+  }
 #pragma unroll
-  for (int c = 0; c < BKV / 32; ++c) {
+  for (int c = 1; c < BKV / 32; ++c) {
     uint32_t (&rc)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[32 * c]);
     tmem_ld_32x32b_x32(s_tm + 32 * c, rc);
   }
@@ -174,10 +195,11 @@ MMK_DEV void softmax_tile(uint32_t s_tm, uint32_t o_tm, uint32_t p_tm, uint64_t*
     uint32_t (&rc)[16] = *reinterpret_cast<uint32_t(*)[16]>(&r[BKV - 16]);
     tmem_ld_32x32b_x16(s_tm + BKV - 16, rc);
   }
-  tmem_ld_wait();
-  tc_fence_before();
-  __syncwarp();
-  if (lane == 0) mbar_arrive(s_free);  // TMEM S_t may now be overwritten by the next S_t
+  if (!pipelined) {
+    tmem_ld_wait();
+    reg_fence<BKV>(r);
+    release_s();
+  }
   if (trace) { TR(t, j, 2) }
   if (valid < BKV) {                   // last tile only (uniform branch)
 #pragma unroll
@@ -237,7 +259,15 @@ MMK_DEV void softmax_tile(uint32_t s_tm, uint32_t o_tm, uint32_t p_tm, uint64_t*
     if (i & 1) sb = __fadd2_rn(sb, e); else sa = __fadd2_rn(sa, e);
     p[i] = pack_bf16x2(e.x, e.y);
   };
-  if (valid >= BKV) {
+  if (pipelined) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) exp_pair(i);
+    tmem_ld_wait();
+    reg_fence<BKV>(r);
+    release_s();
+#pragma unroll
+    for (int i = 16; i < BKV / 2; ++i) exp_pair(i);
+  } else if (valid >= BKV) {
 #pragma unroll
     for (int i = 0; i < BKV / 2; ++i) exp_pair(i);
   } else {
