@@ -392,7 +392,8 @@ def main():
         # dominant kernel = largest share of the (instrumented) step time
         dominant = "attention" if a["ms"] > g["ms"] else "gemm"
         names = {"gemm": "mmk gemm_bf16_tcgen05(_2sm): persistent TMA + tcgen05 (CTA pairs), fused epilogues",
-                 "attention": "mmk attn_fwd_tc: varlen flash attention, S/O in TMEM, tcgen05 + TMA"}
+                 "attention": "mmk attn_fwd_tc(_persistent): varlen flash attention, S/O/P in TMEM, tcgen05 + TMA, "
+                              "speculative row max"}
 
         def roof_entry(kind):
             k = g if kind == "gemm" else a
