@@ -133,36 +133,46 @@ embed_kernel(const float* __restrict__ patch_out, const int32_t* __restrict__ ti
 // One CTA per token row: final fp32 -> bf16 columns [0, d); intermediates interleaved
 // (column d + c*n_inter + j = inter[j][row][c]) staged through shared memory so that both
 // the gather and the 16-byte stores are coalesced.
-__global__ void __launch_bounds__(128)
-pack_mllama_kernel(const float* __restrict__ fin, const __nv_bfloat16* __restrict__ inter, int n_inter, int rows,
-                   int d, __nv_bfloat16* __restrict__ out) {
+// One thread per (token row, group of 8 columns): the 8 final-hidden values (fp32 -> bf16) and,
+// for each of the NI intermediate layers, 8 bf16 values loaded as one 16-byte vector, interleaved
+// in registers into the 8*NI contiguous output values (column d + c*NI + j) and written as NI
+// 16-byte stores — no shared memory, coalesced along the row.
+template <int NI>
+__global__ void __launch_bounds__(256)
+pack_mllama_kernel(const float* __restrict__ fin, const __nv_bfloat16* __restrict__ inter, int rows, int d,
+                   __nv_bfloat16* __restrict__ out) {
   griddep_wait();  // PDL: inputs come from the preceding kernel
   griddep_launch_dependents();
-  extern __shared__ __align__(16) __nv_bfloat16 s_inter[];  // [n_inter][d]
-  const int64_t row = blockIdx.x;
-  const int64_t ldo = static_cast<int64_t>(d) * (1 + n_inter);
-  for (int j = 0; j < n_inter; ++j)
-    for (int c = threadIdx.x * 8; c < d; c += 128 * 8)
-      *reinterpret_cast<uint4*>(s_inter + j * d + c) =
-          *reinterpret_cast<const uint4*>(inter + (static_cast<int64_t>(j) * rows + row) * d + c);
+  const int groups = d / 8;
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<int64_t>(rows) * groups) return;
+  const int64_t row = idx / groups;
+  const int c = static_cast<int>(idx - row * groups) * 8;
+  const int64_t ldo = static_cast<int64_t>(d) * (1 + NI);
   __nv_bfloat16* o = out + row * ldo;
-  for (int c = threadIdx.x * 8; c < d; c += 128 * 8) {
-    const float4 a = *reinterpret_cast<const float4*>(fin + row * d + c);
-    const float4 b = *reinterpret_cast<const float4*>(fin + row * d + c + 4);
-    st_global_v4(o + c, pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y), pack_bf16x2(b.z, b.w));
-  }
-  __syncthreads();
-  const int span = d * n_inter;
-  for (int e = threadIdx.x * 8; e < span; e += 128 * 8) {
-    uint32_t w4[4];
+  const float4 a = __ldg(reinterpret_cast<const float4*>(fin + row * d + c));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(fin + row * d + c + 4));
+  st_global_v4(o + c, pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y), pack_bf16x2(b.z, b.w));
+  if constexpr (NI > 0) {
+    uint16_t v[NI][8];
 #pragma unroll
-    for (int u = 0; u < 8; u += 2) {
-      const int e0 = e + u, e1 = e + u + 1;
-      const __nv_bfloat16 v0 = s_inter[(e0 % n_inter) * d + e0 / n_inter];
-      const __nv_bfloat16 v1 = s_inter[(e1 % n_inter) * d + e1 / n_inter];
-      w4[u / 2] = static_cast<uint32_t>(__bfloat16_as_ushort(v0)) | (static_cast<uint32_t>(__bfloat16_as_ushort(v1)) << 16);
+    for (int j = 0; j < NI; ++j) {
+      const uint4 q = __ldg(reinterpret_cast<const uint4*>(inter + (static_cast<int64_t>(j) * rows + row) * d + c));
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        v[j][2 * k] = static_cast<uint16_t>(w[k] & 0xFFFFu);
+        v[j][2 * k + 1] = static_cast<uint16_t>(w[k] >> 16);
+      }
     }
-    st_global_v4(o + d + e, w4[0], w4[1], w4[2], w4[3]);
+    // output element e (0 .. 8*NI) of this group = column c + e / NI, layer e % NI
+    uint32_t ow[4 * NI];
+#pragma unroll
+    for (int e = 0; e < 8 * NI; e += 2)
+      ow[e / 2] = static_cast<uint32_t>(v[e % NI][e / NI]) | (static_cast<uint32_t>(v[(e + 1) % NI][(e + 1) / NI]) << 16);
+    __nv_bfloat16* oi = o + d + static_cast<int64_t>(c) * NI;
+#pragma unroll
+    for (int k = 0; k < NI; ++k) st_global_v4(oi + 8 * k, ow[4 * k], ow[4 * k + 1], ow[4 * k + 2], ow[4 * k + 3]);
   }
 }
 
@@ -272,14 +282,20 @@ extern "C" int mmk_embed_tokens(const float* patch_out, const int32_t* tile_imag
 extern "C" int mmk_pack_mllama(const float* final_resid, const void* inter, int32_t n_inter, int32_t rows, int32_t d,
                                void* out, cudaStream_t stream) {
   if (rows < 0 || d <= 0 || n_inter < 0 || d % 8 != 0) return set_error(MMK_ERR_ARG, "pack_mllama: bad shape");
+  if (n_inter > 8) return set_error(MMK_ERR_UNSUPPORTED, "pack_mllama: n_inter=%d > 8", n_inter);
   if (rows == 0) return MMK_OK;
-  const int smem = n_inter * d * 2;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(pack_mllama_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return set_cuda_error(e, "pack_mllama: smem attr");
+  const int64_t items = static_cast<int64_t>(rows) * (d / 8);
+  const dim3 grid(static_cast<unsigned>((items + 255) / 256));
+  const auto* in = reinterpret_cast<const __nv_bfloat16*>(inter);
+  auto* o = reinterpret_cast<__nv_bfloat16*>(out);
+  const bool small = rows <= kSmallRows;
+  switch (n_inter) {
+#define MMK_PACK_CASE(N) \
+  case N: (void)launch_kernel(pack_mllama_kernel<N>, grid, dim3(256), 0, stream, 1, small, final_resid, in, rows, d, o); break;
+    MMK_PACK_CASE(0) MMK_PACK_CASE(1) MMK_PACK_CASE(2) MMK_PACK_CASE(3) MMK_PACK_CASE(4)
+    MMK_PACK_CASE(5) MMK_PACK_CASE(6) MMK_PACK_CASE(7) MMK_PACK_CASE(8)
+#undef MMK_PACK_CASE
   }
-  (void)launch_kernel(pack_mllama_kernel, dim3(rows), dim3(128), smem, stream, 1, rows <= kSmallRows, final_resid, reinterpret_cast<const __nv_bfloat16*>(inter), n_inter,
-                                                  rows, d, reinterpret_cast<__nv_bfloat16*>(out));
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "pack_mllama: launch");
 }

@@ -253,9 +253,10 @@ def test_layernorm_and_tile_add(mk):
     torch.testing.assert_close(y, ref, rtol=1e-4, atol=1e-4)
 
 
-def test_pack_mllama_layout(mk):
+@pytest.mark.parametrize("n_inter,d", [(5, 1280), (1, 1280), (3, 64), (8, 256)])
+def test_pack_mllama_layout(mk, n_inter, d):
     _, ops, _ = mk
-    rows, d, n_inter = 333, 1280, 5
+    rows = 333
     fin = torch.randn(rows, d, device="cuda")
     inter = torch.randn(n_inter, rows, d, device="cuda").bfloat16()
     out = ops.pack_mllama(fin, inter)
