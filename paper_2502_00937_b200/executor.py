@@ -85,24 +85,37 @@ def stage_images(images, device="cuda", pinned: bool = True, stream=None) -> Ima
     dev = torch.device(device)
     meta = np.concatenate([offs.view(np.int32), np.array([d[0] for d in dims], np.int32),
                            np.array([d[1] for d in dims], np.int32)]) if imgs else np.zeros(0, np.int32)
-    host = torch.empty(total, dtype=torch.uint8, pin_memory=pinned)
-    hv = host.numpy()
-    for i, im in enumerate(imgs):
-        a = im.cpu().numpy() if isinstance(im, torch.Tensor) else im
-        hv[offs[i]:offs[i] + sizes[i]] = a.reshape(-1)
+    # images already in pinned host tensors (a decoder writing straight into page-locked memory)
+    # are copied to the device one by one, without a host-side concatenation
+    direct = bool(imgs) and all(isinstance(i, torch.Tensor) and i.device.type == "cpu" and i.is_pinned()
+                                and i.is_contiguous() for i in imgs)
+    host = None
+    if not direct:
+        host = torch.empty(total, dtype=torch.uint8, pin_memory=pinned)
+        hv = host.numpy()
+        for i, im in enumerate(imgs):
+            a = im.cpu().numpy() if isinstance(im, torch.Tensor) else im
+            hv[offs[i]:offs[i] + sizes[i]] = a.reshape(-1)
     hmeta = torch.from_numpy(meta)
     if pinned:
         hmeta = hmeta.pin_memory()
+
+    def copy_in():
+        if direct:
+            dst = torch.empty(total, dtype=torch.uint8, device=dev)
+            for i, im in enumerate(imgs):
+                dst[offs[i]:offs[i] + sizes[i]].copy_(im.view(-1), non_blocking=True)
+            return dst, hmeta.to(dev, non_blocking=True)
+        return host.to(dev, non_blocking=True), hmeta.to(dev, non_blocking=True)
+
     ready = None
     if stream is not None:
         with torch.cuda.stream(stream):
-            src = host.to(dev, non_blocking=True)
-            dmeta = hmeta.to(dev, non_blocking=True)
+            src, dmeta = copy_in()
             ready = torch.cuda.Event()
             ready.record(stream)
     else:
-        src = host.to(dev, non_blocking=True)
-        dmeta = hmeta.to(dev, non_blocking=True)
+        src, dmeta = copy_in()
     n = len(imgs)
     src_off = dmeta[:2 * n].view(torch.int64)
     return ImageBatch(src=src, src_off=src_off, w=dmeta[2 * n:3 * n], h=dmeta[3 * n:4 * n], dims=dims,

@@ -349,8 +349,11 @@ def test_stage_images_side_stream_matches(mk):
     b2 = stage_images(imgs, stream=side)
     o1 = ex.encode(b1)
     o2 = ex.encode(b2)
+    pinned = [torch.from_numpy(i).pin_memory() for i in imgs]  # per-image H2D, no host concatenation
+    o3 = ex.encode(stage_images(pinned, stream=side))
     torch.cuda.synchronize()
     assert torch.equal(o1.embeds, ref.embeds) and torch.equal(o2.embeds, ref.embeds)
+    assert torch.equal(o3.embeds, ref.embeds)
 
 
 def test_plain_c_client_of_the_abi(mk):
