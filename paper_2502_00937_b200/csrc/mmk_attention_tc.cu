@@ -506,7 +506,10 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
 // ---------------------------------------------------------------------------- persistent form
 // One CTA per SM takes work items — (query block of NQ*128 rows, head, sequence), query block
 // fastest, the heads of one image adjacent — from a global counter, so ragged batches balance
-// dynamically.  The TMA warp fetches and decodes each item and hands it to the other warps
+// dynamically.  With n_seq <= kMaxSched the sequences are visited longest first (LPT order: the
+// last items to start are the cheapest, which shortens the tail) and only non-empty query blocks
+// are items; the TMA warp of every CTA builds the same order (a rank sort over the lengths) and
+// the per-sequence item prefix in shared memory at start-up.  The TMA warp fetches and decodes each item and hands it to the other warps
 // through a 4-deep shared-memory ring; every role therefore walks the same item sequence, and the
 // next item's Q (double-buffered) and first K/V tiles load, and its first S = Q K^T runs, while
 // the previous item's last softmax, PV and output store are in flight.  Barrier phases run on
@@ -517,6 +520,8 @@ struct AttnItem {
   int s_begin, len, q0, head, n_qt, nkv;  // len < 0: no more items
 };
 
+constexpr int kMaxSched = 256;
+
 template <int HD, int BKV, int NQ>
 struct TcPersistLayout {
   using C = TcAttnCfg<HD, BKV, NQ>;
@@ -524,7 +529,10 @@ struct TcPersistLayout {
   static constexpr int kQOff = 0;                          // two Q slots
   static constexpr int kKVOff = 2 * kQSlotBytes;
   static constexpr int kBarOff = kKVOff + C::STAGES * C::kStageBytes;
-  static constexpr int kSmem = kBarOff + 512 + 1024;
+  // longest-first schedule (n_seq <= kMaxSched): lengths, sorted order, item prefix
+  static constexpr int kSchedOff = kBarOff + 512;
+  static constexpr int kSchedBytes = (3 * kMaxSched + 1) * 4;
+  static constexpr int kSmem = kSchedOff + kSchedBytes + 1024;
   static_assert((12 + 3 * C::STAGES + 5 * NQ) * 8 + 4 * sizeof(AttnItem) + 4 <= 512, "barrier area");
   static_assert(kSmem <= 232448, "shared memory overflow");
 };
@@ -537,7 +545,7 @@ attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_co
                        const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_kv_rem,
                        __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ cu_seqlens, int n_seq,
                        int heads, int qblocks, float scale_log2, int* __restrict__ item_counter,
-                       int* __restrict__ overflow_flag, const int* __restrict__ gate) {
+                       int* __restrict__ overflow_flag, const int* __restrict__ gate, bool lpt) {
   if (gate != nullptr) {  // the flag is written by the speculative pass just before (PDL)
     griddep_wait();
     if (*reinterpret_cast<const volatile int*>(gate) == 0) return;
@@ -563,8 +571,11 @@ attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_co
   AttnItem* ring = reinterpret_cast<AttnItem*>(item_empty + 4);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + 4);
 
-  const int n_items = qblocks * heads * n_seq;
+  int n_items = qblocks * heads * n_seq;
   const int d_model = heads * HD;
+  int* sch_len = reinterpret_cast<int*>(smem + Lay::kSchedOff);  // [kMaxSched]
+  int* sch_order = sch_len + kMaxSched;                           // [kMaxSched] rank -> sequence
+  int* sch_pre = sch_order + kMaxSched;                           // [kMaxSched + 1] items before rank
   const uint32_t warp = warp_id_uniform();
   const uint32_t lane = lane_id();
 
@@ -623,15 +634,59 @@ attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_co
 
   if (warp == kTmaWarp) {
     // ---------------------------------------------------------------- scheduler + TMA producer
+    if (lpt) {
+      for (int i = lane; i < n_seq; i += 32) sch_len[i] = __ldg(cu_seqlens + i + 1) - __ldg(cu_seqlens + i);
+      __syncwarp();
+      for (int i = lane; i < n_seq; i += 32) {  // rank = #longer + #equal with a lower index
+        const int li = sch_len[i];
+        int r = 0;
+        for (int j = 0; j < n_seq; ++j) {
+          const int lj = sch_len[j];
+          r += (lj > li) | ((lj == li) & (j < i));
+        }
+        sch_order[r] = i;
+      }
+      __syncwarp();
+      int carry = 0;
+      if (lane == 0) sch_pre[0] = 0;
+      for (int base = 0; base < n_seq; base += 32) {  // warp scan of the per-sequence item counts
+        const int r = base + static_cast<int>(lane);
+        int v = r < n_seq ? (sch_len[sch_order[r]] + NQ * kTcBQ - 1) / (NQ * kTcBQ) * heads : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int u = __shfl_up_sync(0xffffffffu, v, o);
+          if (lane >= static_cast<uint32_t>(o)) v += u;
+        }
+        if (r < n_seq) sch_pre[r + 1] = carry + v;
+        carry += __shfl_sync(0xffffffffu, v, 31);
+      }
+      __syncwarp();
+      n_items = carry;
+    }
     if (elect_one()) {
       uint32_t kv = 0, qi = 0;
       for (uint32_t k = 0;; ++k) {
         const int item = atomicAdd(item_counter, 1);
         AttnItem it{0, -1, 0, 0, 0, 0};
         if (item < n_items) {
-          const int qb = item % qblocks, rest = item / qblocks;
-          it.head = rest % heads;
-          const int seq = rest / heads;
+          int qb, seq;
+          if (lpt) {
+            int lo = 0, hi = n_seq;  // largest lo with sch_pre[lo] <= item
+            while (hi - lo > 1) {
+              const int mid = (lo + hi) >> 1;
+              if (sch_pre[mid] <= item) lo = mid; else hi = mid;
+            }
+            seq = sch_order[lo];
+            const int local = item - sch_pre[lo];
+            const int nqb = (sch_len[seq] + NQ * kTcBQ - 1) / (NQ * kTcBQ);
+            qb = local % nqb;
+            it.head = local / nqb;
+          } else {
+            qb = item % qblocks;
+            const int rest = item / qblocks;
+            it.head = rest % heads;
+            seq = rest / heads;
+          }
           it.s_begin = __ldg(cu_seqlens + seq);
           it.len = __ldg(cu_seqlens + seq + 1) - it.s_begin;
           it.q0 = qb * NQ * kTcBQ;
@@ -791,6 +846,11 @@ static int launch_attn_cfg(const void* qkv, void* out, const int32_t* cu, int n_
   const int qblocks = (max_s + NQ * kTcBQ - 1) / (NQ * kTcBQ);
   const int64_t n_items = static_cast<int64_t>(qblocks) * heads * n_seq;
   if (n_items >= INT32_MAX) return set_error(MMK_ERR_UNSUPPORTED, "attention_tc: too many work items");
+  static const bool lpt_on = [] {
+    const char* e = getenv("MMK_ATTN_LPT");
+    return e ? atoi(e) != 0 : true;
+  }();
+  const bool lpt = lpt_on && n_seq <= kMaxSched;
   const int persist_grid = static_cast<int>(n_items < num_sms() ? n_items : num_sms());  // one CTA per SM
   __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out);
   // workspace: [0] work-item counter of the main pass, [1] overflow flag, [2] counter of the exact redo
@@ -809,7 +869,7 @@ static int launch_attn_cfg(const void* qkv, void* out, const int32_t* cu, int n_
   if constexpr (PERSIST) {
     me = launch_kernel(attn_fwd_tc_persistent<HD, BKV, NQ, SPEC>, dim3(persist_grid), dim3(C::kThreads), Lay::kSmem,
                        stream, 1, false, tq, tqr, tkv, tkvr, o, cu, n_seq, heads, qblocks, scale_log2, ws, ws + 1,
-                       static_cast<const int*>(nullptr));
+                       static_cast<const int*>(nullptr), lpt);
     if (me != cudaSuccess) return set_cuda_error(me, "attention_tc: launch");
   } else {
     static std::atomic<uint64_t> attr_done{0};
@@ -825,7 +885,7 @@ static int launch_attn_cfg(const void* qkv, void* out, const int32_t* cu, int n_
     // exact redo of the whole launch, gated on the overflow flag (all CTAs exit at once when clear)
     me = launch_kernel(attn_fwd_tc_persistent<HD, BKV, NQ, false>, dim3(persist_grid), dim3(C::kThreads),
                        Lay::kSmem, stream, 1, !PERSIST, tq, tqr, tkv, tkvr, o, cu, n_seq, heads, qblocks, scale_log2, ws + 2,
-                       static_cast<int*>(nullptr), static_cast<const int*>(ws + 1));
+                       static_cast<int*>(nullptr), static_cast<const int*>(ws + 1), lpt);
     if (me != cudaSuccess) return set_cuda_error(me, "attention_tc: launch");
   }
   cudaError_t e = cudaGetLastError();

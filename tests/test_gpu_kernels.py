@@ -191,7 +191,12 @@ def _attn_ref(qkv, lens, heads, hd):
 @pytest.mark.parametrize("hd,heads,lens", [(80, 16, [1601, 3202, 1, 63, 64, 65, 6404]),
                                            (64, 16, [577, 577, 129]), (64, 12, [197] * 8), (80, 4, [17, 4803]),
                                            (80, 16, [1601] * 40 + [3202] * 4),    # persistent (> 2 waves)
-                                           (64, 16, [0, 577, 0, 5, 577] * 12)])   # empty sequences mixed in
+                                           (64, 16, [0, 577, 0, 5, 577] * 12),    # empty sequences mixed in
+                                           # ragged Mllama-like mix: longest-first persistent schedule
+                                           (80, 16, [1601 * t for t in (1, 4, 2, 3, 1, 1, 4, 2) * 4]),
+                                           # n_seq == 256 (largest sorted schedule), lengths 0..700 with ties
+                                           (64, 4, [(i * 37) % 701 for i in range(256)]),
+                                           (64, 12, [197] * 300)])                # n_seq > 256: natural order
 def test_attention_varlen(mk, hd, heads, lens):
     _, ops, _ = mk
     T = sum(lens)
