@@ -49,6 +49,12 @@ def run(lens, heads, hd, iters=10, check=True):
 
 if __name__ == "__main__":
     print("impl:", "legacy mma.sync" if os.environ.get("MMK_ATTN_LEGACY") else "tcgen05", os.environ.get("MMK_LIB", ""))
+    if os.environ.get("ATTN_PROBE_HD64"):
+        run([577, 577, 129, 1, 64, 65, 200], 16, 64)
+        run([577] * 256, 16, 64, check=False)
+        run([197] * 64, 12, 64, check=False)
+        run([197] * 256, 12, 64, check=False)
+        sys.exit(0)
     if os.environ.get("ATTN_PROBE_QUICK"):
         run([t * 1601 for t in BENCH_MIX], 16, 80, check=False)
         run([6404] * 8, 16, 80, check=False)
