@@ -13,8 +13,10 @@
  *   LatencyProfile.encode_latency       profiles.py:136-145        mmk_gemm_bf16 / mmk_layernorm_f32
  *                                                                  / mmk_attention_varlen_bf16 /
  *                                                                  mmk_embed_* (K2-K8)
- *   shard join + handoff                engine.py:730-752, :563-579 mmk_pack_* (K9) + NCCL P2P (K10,
- *                                                                  host side, torch.distributed)
+ *   shard join + handoff                engine.py:730-752, :563-579 mmk_pack_mllama_peer (K9+K10 fused:
+ *                                                                  pack straight into the LLM GPU's
+ *                                                                  memory over NVLink) or mmk_pack_*
+ *                                                                  + NCCL P2P (host side)
  *
  * Conventions (all functions):
  *   - return int status: MMK_OK, MMK_ERR_ARG (-> SpecError), MMK_ERR_UNSUPPORTED
@@ -146,6 +148,16 @@ int mmk_embed_tokens(const float* patch_out, const int32_t* tile_image, const in
  */
 int mmk_pack_mllama(const float* final_resid, const void* inter, int32_t n_inter, int32_t rows,
                     int32_t d, void* out, cudaStream_t stream);
+/*
+ * K9 + K10 fused: the same layout as mmk_pack_mllama, for an `out` that may live in another GPU's
+ * memory (a CUDA peer / symmetric-memory mapping of the LLM-backend GPU's receive buffer —
+ * replaces the pack + NCCL send of the shard handoff, engine.py:563-579 / :730-752).  Each CTA
+ * assembles whole output rows in shared memory and moves each row with one bulk copy, so the
+ * NVLink fabric sees contiguous full-line writes.  out: 16-byte aligned.  The writes are complete
+ * when the stream reaches the end of this call (signal the receiver after it, e.g. with an event).
+ */
+int mmk_pack_mllama_peer(const float* final_resid, const void* inter, int32_t n_inter, int32_t rows,
+                         int32_t d, void* out, cudaStream_t stream);
 /*
  * CLIP/LLaVA: drop the first `drop` tokens of every tile: out bf16 [tiles*(P-drop), d] from
  * src (bf16 or f32 when src_f32 != 0) [tiles*P, d].

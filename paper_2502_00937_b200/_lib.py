@@ -40,6 +40,7 @@ SIGNATURES = {
     "mmk_embed_tokens": ([_V, _V, _V, _V, _I32, _I32, _I32, _V, _V, _F, _V, _F, _V, _F, _I32, _V, _V, _F, _V, _V],
                          _I32),
     "mmk_pack_mllama": ([_V, _V, _I32, _I32, _I32, _V, _V], _I32),
+    "mmk_pack_mllama_peer": ([_V, _V, _I32, _I32, _I32, _V, _V], _I32),
     "mmk_pack_drop_cls": ([_V, _I32, _I32, _I32, _I32, _I32, _V, _V], _I32),
     "mmk_checksum_bf16": ([_V, _I64, _V, _V], _I32),
 }

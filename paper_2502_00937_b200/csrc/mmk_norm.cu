@@ -176,6 +176,80 @@ pack_mllama_kernel(const float* __restrict__ fin, const __nv_bfloat16* __restric
   }
 }
 
+// K9 + K10 fused: the same packing, written to a destination that may live in another GPU's
+// memory (NVLink peer mapping / symmetric memory).  Each CTA assembles whole output rows in shared
+// memory and moves them out as one contiguous span per row — `BULK`: one cp.async.bulk copy per
+// row, issued by one thread; else 16-byte stores with a warp covering 512 contiguous bytes — so
+// the fabric sees full-line writes instead of the 80-byte-strided stores of the direct kernel.
+// Rows are double-buffered: row i+1 is assembled while row i drains.
+template <int NI, bool BULK>
+__global__ void __launch_bounds__(256)
+pack_mllama_staged_kernel(const float* __restrict__ fin, const __nv_bfloat16* __restrict__ inter, int rows, int d,
+                          __nv_bfloat16* __restrict__ out) {
+  extern __shared__ __align__(128) uint8_t pk_smem[];
+  griddep_wait();
+  griddep_launch_dependents();
+  const int groups = d / 8;
+  const int64_t ldo = static_cast<int64_t>(d) * (1 + NI);
+  const int row_bytes = static_cast<int>(ldo * 2);
+  const int row_vec = row_bytes / 16;
+  int buf = 0;
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x, buf ^= 1) {
+    uint8_t* sm = pk_smem + buf * row_bytes;
+    if constexpr (BULK) {  // the copy that last read this buffer (two rows ago) has drained
+      if (threadIdx.x == 0) tma_store_wait_read<1>();
+      __syncthreads();
+    }
+    for (int g = threadIdx.x; g < groups; g += blockDim.x) {
+      const int c = g * 8;
+      const float4 a = __ldg(reinterpret_cast<const float4*>(fin + row * d + c));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(fin + row * d + c + 4));
+      *reinterpret_cast<uint4*>(sm + c * 2) =
+          make_uint4(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y), pack_bf16x2(b.z, b.w));
+      if constexpr (NI > 0) {
+        uint16_t v[NI][8];
+#pragma unroll
+        for (int j = 0; j < NI; ++j) {
+          const uint4 q = __ldg(reinterpret_cast<const uint4*>(inter + (static_cast<int64_t>(j) * rows + row) * d + c));
+          const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            v[j][2 * k] = static_cast<uint16_t>(w[k] & 0xFFFFu);
+            v[j][2 * k + 1] = static_cast<uint16_t>(w[k] >> 16);
+          }
+        }
+        uint32_t ow[4 * NI];
+#pragma unroll
+        for (int e = 0; e < 8 * NI; e += 2)
+          ow[e / 2] = static_cast<uint32_t>(v[e % NI][e / NI]) | (static_cast<uint32_t>(v[(e + 1) % NI][(e + 1) / NI]) << 16);
+        uint4* si = reinterpret_cast<uint4*>(sm + (d + c * NI) * 2);
+#pragma unroll
+        for (int k = 0; k < NI; ++k) si[k] = make_uint4(ow[4 * k], ow[4 * k + 1], ow[4 * k + 2], ow[4 * k + 3]);
+      }
+    }
+    if constexpr (BULK) {
+      fence_proxy_async();  // generic-proxy smem writes -> visible to the bulk copy
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + row * ldo),
+                     "r"(smem_u32(sm)), "r"(row_bytes)
+                     : "memory");
+        tma_store_commit();
+      }
+    } else {
+      __syncthreads();
+      const uint4* src = reinterpret_cast<const uint4*>(sm);
+      uint4* dst = reinterpret_cast<uint4*>(out + row * ldo);
+      for (int i = threadIdx.x; i < row_vec; i += blockDim.x) dst[i] = src[i];
+      // the next row assembles into the other buffer; this one is rewritten two rows on, after the
+      // __syncthreads that precedes that row's copy-out
+    }
+  }
+  if constexpr (BULK) {
+    if (threadIdx.x == 0) tma_store_wait<0>();  // writes complete before the kernel retires
+  }
+}
+
 __global__ void __launch_bounds__(256)
 pack_drop_kernel(const void* __restrict__ src, int src_f32, int64_t out_rows, int tokens_per_tile, int drop, int d,
                  __nv_bfloat16* __restrict__ out) {
@@ -298,6 +372,37 @@ extern "C" int mmk_pack_mllama(const float* final_resid, const void* inter, int3
   }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "pack_mllama: launch");
+}
+
+extern "C" int mmk_pack_mllama_peer(const float* final_resid, const void* inter, int32_t n_inter, int32_t rows,
+                                    int32_t d, void* out, cudaStream_t stream) {
+  if (rows < 0 || d <= 0 || n_inter < 0 || d % 8 != 0) return set_error(MMK_ERR_ARG, "pack_mllama_peer: bad shape");
+  if (n_inter > 8) return set_error(MMK_ERR_UNSUPPORTED, "pack_mllama_peer: n_inter=%d > 8", n_inter);
+  if (reinterpret_cast<uintptr_t>(out) % 16 != 0) return set_error(MMK_ERR_ARG, "pack_mllama_peer: out not 16-byte aligned");
+  if (rows == 0) return MMK_OK;
+  static const int mode = [] {
+    const char* e = getenv("MMK_PACK_PEER_BULK");
+    return e ? atoi(e) : 1;
+  }();
+  const int smem = 2 * d * (1 + n_inter) * 2;
+  if (smem > 200 * 1024) return set_error(MMK_ERR_UNSUPPORTED, "pack_mllama_peer: row of %d bytes", smem / 2);
+  const dim3 grid(static_cast<unsigned>(rows < 4 * num_sms() ? rows : 4 * num_sms()));
+  const auto* in = reinterpret_cast<const __nv_bfloat16*>(inter);
+  auto* o = reinterpret_cast<__nv_bfloat16*>(out);
+  cudaError_t e = cudaSuccess;
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) e = launch_kernel(kern, grid, dim3(256), smem, stream, 1, false, final_resid, in, rows, d, o);
+  };
+  switch (n_inter) {
+#define MMK_PACK_CASE(N) \
+  case N: if (mode) go(pack_mllama_staged_kernel<N, true>); else go(pack_mllama_staged_kernel<N, false>); break;
+    MMK_PACK_CASE(0) MMK_PACK_CASE(1) MMK_PACK_CASE(2) MMK_PACK_CASE(3) MMK_PACK_CASE(4)
+    MMK_PACK_CASE(5) MMK_PACK_CASE(6) MMK_PACK_CASE(7) MMK_PACK_CASE(8)
+#undef MMK_PACK_CASE
+  }
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "pack_mllama_peer: launch");
 }
 
 extern "C" int mmk_pack_drop_cls(const void* src, int32_t src_f32, int32_t tiles, int32_t tokens_per_tile,

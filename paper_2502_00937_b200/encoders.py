@@ -157,9 +157,11 @@ class DeviceEncoder:
         ops.gemm(h_buf, L["fc2_w"], ops.EPI_RESID_F32, bias=L["fc2_b"], out=resid, gate=L["gate_ffn"], aux=aux)
 
     def forward(self, patches: torch.Tensor, total_tiles: int, cu_seqlens: torch.Tensor, n_seq: int, max_seqlen: int,
-                tile_image=None, tile_slot=None, image_ar=None) -> torch.Tensor:
+                tile_image=None, tile_slot=None, image_ar=None, out_alloc=None) -> torch.Tensor:
         """patches [total_tiles*P, k_pad] bf16 -> packed embeddings for the LLM prefill.
-        cu_seqlens int32 [n_seq+1] token offsets of the attention sequences (one per image)."""
+        cu_seqlens int32 [n_seq+1] token offsets of the attention sequences (one per image).
+        out_alloc(rows, width) -> bf16 tensor: destination of the packed output, possibly in the
+        LLM-backend GPU's memory (peer view); the pack then streams whole rows over NVLink."""
         enc, P, d = self.enc, self.P, self.enc.hidden
         dev = patches.device
         T = total_tiles * (P + 1)
@@ -180,10 +182,13 @@ class DeviceEncoder:
             for L in self.layers[:n_run]:
                 self._block(L, resid, x_buf, qkv_buf, h_buf, cu_seqlens, n_seq, max_seqlen)
             drop = 1 if enc.drop_cls else 0
+            dst = out_alloc(total_tiles * (P + 1 - drop), d) if out_alloc is not None else None
             if enc.out_layer == -1:
+                if drop == 0:
+                    return ops.layernorm(resid, *self.post_ln, enc.norm_eps, out=x_buf if dst is None else dst)
                 ops.layernorm(resid, *self.post_ln, enc.norm_eps, out=x_buf)
-                return x_buf if drop == 0 else ops.pack_drop_cls(x_buf, total_tiles, P + 1, drop)
-            return ops.pack_drop_cls(resid, total_tiles, P + 1, drop)
+                return ops.pack_drop_cls(x_buf, total_tiles, P + 1, drop, out=dst)
+            return ops.pack_drop_cls(resid, total_tiles, P + 1, drop, out=dst)
         # ---------------- mllama
         outs = list(enc.out_layers)
         if 0 in outs:
@@ -199,4 +204,6 @@ class DeviceEncoder:
         for L in self.global_layers:
             self._block(L, resid, x_buf, qkv_buf, h_buf, cu_seqlens, n_seq, max_seqlen)
         del x_buf, qkv_buf, h_buf
+        if out_alloc is not None:
+            return ops.pack_mllama(resid, inter, out=out_alloc(T, d * (1 + len(outs))), peer=True)
         return ops.pack_mllama(resid, inter)

@@ -190,7 +190,9 @@ class ImagePathExecutor:
         self.encoder = DeviceEncoder(spec, self.weights, self.device)
 
     # ------------------------------------------------------------------ core path
-    def encode(self, batch: ImageBatch) -> PackedBatch:
+    def encode(self, batch: ImageBatch, out_alloc=None) -> PackedBatch:
+        """out_alloc(rows, width) (optional): where the packed output goes (e.g. a slot of the
+        LLM-backend GPU's memory, PeerShardChannel.alloc); default a fresh local tensor."""
         spec, enc = self.spec, self.spec.encoder
         n = batch.n
         if n == 0:
@@ -214,9 +216,10 @@ class ImagePathExecutor:
         max_s = int(max(tiles)) * (P + 1)
         if enc.family == "mllama":
             tile_image, tile_slot = ops.tile_index(plan["tile_off"], n, total_tiles)
-            emb = self.encoder.forward(patches, total_tiles, cu, n, max_s, tile_image, tile_slot, plan["ar_id"])
+            emb = self.encoder.forward(patches, total_tiles, cu, n, max_s, tile_image, tile_slot, plan["ar_id"],
+                                       out_alloc=out_alloc)
         else:
-            emb = self.encoder.forward(patches, total_tiles, cu, n, max_s)
+            emb = self.encoder.forward(patches, total_tiles, cu, n, max_s, out_alloc=out_alloc)
         return PackedBatch(embeds=emb, tok_offsets=plan["tok_off"], tiles=tiles,
                            image_tokens=[t * spec.tokens_per_tile for t in tiles])
 
@@ -230,15 +233,15 @@ class ImagePathExecutor:
             out = self.encode(batch)
         return CapturedEncode(graph=g, batch=batch, output=out)
 
-    def encode_images(self, images, pinned: bool = True) -> PackedBatch:
-        return self.encode(stage_images(images, self.device, pinned))
+    def encode_images(self, images, pinned: bool = True, out_alloc=None) -> PackedBatch:
+        return self.encode(stage_images(images, self.device, pinned), out_alloc=out_alloc)
 
     def encode_jpegs(self, jpegs) -> PackedBatch:
         """JPEG bytes -> GPU decode -> K0..K9 (no host pixel handling at all)."""
         return self.encode(stage_jpegs(jpegs, self.device))
 
     # ------------------------------------------------------------------ batcher API
-    def run(self, batch: list[WorkItem], images: dict) -> PackedBatch:
+    def run(self, batch: list[WorkItem], images: dict, out_alloc=None) -> PackedBatch:
         """Execute one ``form_batch`` result of ENCODE (or PREPROCESS) items.
 
         images: request_id -> list of uint8 HWC images of that request; each item's
@@ -254,6 +257,6 @@ class ImagePathExecutor:
             start = len(flat)
             flat.extend(req_imgs[i] for i in idx)
             spans[it.seq] = (start, len(flat))
-        out = self.encode_images(flat)
+        out = self.encode_images(flat, out_alloc=out_alloc)
         out.item_spans = spans
         return out

@@ -213,13 +213,17 @@ def embed_tokens(patch_out, total_tiles: int, patches_per_tile: int, cls, pos, p
     return out
 
 
-def pack_mllama(final_resid, inter, out=None):
+def pack_mllama(final_resid, inter, out=None, peer: bool = False):
+    """K9.  ``peer=True``: ``out`` may be another GPU's memory (a symmetric-memory / P2P view);
+    rows are staged in shared memory and leave as whole contiguous spans (fused pack + NVLink
+    transfer, mmk_pack_mllama_peer)."""
     rows, d = final_resid.shape
     n_inter = inter.shape[0] if inter is not None else 0
     if out is None:
         out = torch.empty(rows, d * (1 + n_inter), dtype=torch.bfloat16, device=final_resid.device)
     _t0 = _begin()
-    _lib.check(_lib.lib.mmk_pack_mllama(final_resid.data_ptr(), _p(inter), n_inter, rows, d, out.data_ptr(), _s()))
+    fn = _lib.lib.mmk_pack_mllama_peer if peer else _lib.lib.mmk_pack_mllama
+    _lib.check(fn(final_resid.data_ptr(), _p(inter), n_inter, rows, d, out.data_ptr(), _s()))
     _end('pack', out.numel() * 2.0 * 2, _t0)
     return out
 

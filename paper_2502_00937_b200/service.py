@@ -105,7 +105,8 @@ class ShardChannel:
         data = {src: dist.new_group([0, src], backend=backend_data) for src in range(1, world)}
         return ctrl, data
 
-    def __init__(self, rank: int, world: int, device, dtype, ctrl_group=None, data_group=None, on_arrival=None):
+    def __init__(self, rank: int, world: int, device, dtype, ctrl_group=None, data_group=None, on_arrival=None,
+                 on_receive=None):
         import queue
         import threading
 
@@ -115,9 +116,11 @@ class ShardChannel:
         self.rank, self.world, self.device, self.dtype = rank, world, device, dtype
         self.ctrl, self.data = ctrl_group, data_group
         self.on_arrival = on_arrival  # runs in the receiver thread, on its private stream
+        self.on_receive = on_receive  # (request id, shard id, rows) hook before on_arrival (checks)
         self.outgoing = []
         self.ready = queue.Queue()
         self.ended = 0
+        self.counts = {"peer": 0, "nccl": 0}  # rank 0: shards received per payload path
         self.threads = []
         if rank == 0:
             for src in range(1, world):
@@ -133,12 +136,17 @@ class ShardChannel:
             torch.cuda.set_device(self.device)
             torch.cuda.set_stream(torch.cuda.Stream(self.device))
         while True:
-            hdr = torch.empty(4, dtype=torch.int64)
+            hdr = torch.empty(self.HDR, dtype=torch.int64)
             dist.recv(hdr, src, group=self._g(self.ctrl, src))
-            rid, sid, rows, width = (int(v) for v in hdr.tolist())
+            rid, sid, rows, width, slot, row0, last, _ = (int(v) for v in hdr.tolist())
             if rid < 0:
                 self.ready.put(None)
                 return
+            if slot >= 0:  # payload already in this GPU's memory (PeerShardChannel)
+                self.counts["peer"] += 1
+                self._peer_arrival(src, rid, sid, rows, width, slot, row0, last)
+                continue
+            self.counts["nccl"] += 1
             buf = torch.empty(rows, width, dtype=self.dtype, device=self.device)
             work = dist.irecv(buf, src, group=self._g(self.data, src))
             if self.device.type == "cuda":
@@ -147,13 +155,20 @@ class ShardChannel:
                     _t.sleep(0.0005)  # coarse poll: keeps the GIL free for the replay loop
             else:
                 work.wait()
+            if self.on_receive is not None:
+                self.on_receive(rid, sid, buf)
             extra = self.on_arrival(buf) if self.on_arrival is not None else None
             if self.device.type == "cuda":
                 buf.record_stream(torch.cuda.default_stream(self.device))  # consumed by the replay loop
             self.ready.put((rid, sid, buf if extra is None else extra))
 
-    def send(self, req_id: int, shard_id: int, emb) -> None:
-        h = self.torch.tensor([req_id, shard_id, emb.shape[0], emb.shape[1]], dtype=self.torch.int64)
+    HDR = 8  # request id, shard id, rows, width, peer slot (-1: NCCL payload follows), first row, last, 0
+
+    def _peer_arrival(self, *args):
+        raise RuntimeError("peer-slot header on a channel without peer slots")
+
+    def send(self, req_id: int, shard_id: int, emb, last: bool = False) -> None:
+        h = self.torch.tensor([req_id, shard_id, emb.shape[0], emb.shape[1], -1, 0, 0, 0], dtype=self.torch.int64)
         self.dist.send(h, 0, group=self._g(self.ctrl, self.rank))
         w2 = self.dist.isend(emb.contiguous(), 0, group=self._g(self.data, self.rank))
         self.outgoing.append((w2, emb))
@@ -178,7 +193,7 @@ class ShardChannel:
         if self.rank != 0:
             for w, _ in self.outgoing:
                 w.wait()
-            self.dist.send(self.torch.tensor([-1, -1, 0, 0], dtype=self.torch.int64), 0,
+            self.dist.send(self.torch.tensor([-1, -1, 0, 0, -1, 0, 0, 0], dtype=self.torch.int64), 0,
                            group=self._g(self.ctrl, self.rank))
         else:
             for th in self.threads:
@@ -190,6 +205,75 @@ class ShardChannel:
     @staticmethod
     def _g(group, src):
         return group.get(src) if isinstance(group, dict) else group
+
+
+class PeerShardChannel(ShardChannel):
+    """ShardChannel whose payload bypasses NCCL (K9 + K10 fused, CUDA only).
+
+    Rank 0 (the LLM-backend rank) owns ``n_slots`` receive slots per source rank in symmetric
+    memory (torch.distributed._symmetric_memory: the same allocation mapped into every rank over
+    NVLink).  A source's encoder packs its batch output straight into its next slot on rank 0
+    (``alloc`` -> a peer view; K9 stages whole rows in shared memory and moves them with bulk
+    copies, mmk_pack_mllama_peer), and once the batch has completed only the int64 header travels
+    (gloo), naming slot and rows.  Rank 0 consumes the rows in place and releases the slot with a
+    stream-ordered signal; the source's stream waits on that signal before packing into the slot
+    again.  Batches larger than a slot fall back to the NCCL payload of the base class.  A tensor
+    that ``poll`` returns for a slot aliases it: valid until the source has packed ``n_slots``
+    more batches (consume it in ``on_receive`` / ``on_arrival``, which run before the release)."""
+
+    def __init__(self, rank: int, world: int, device, dtype, slot_rows: int, width: int, n_slots: int = 2,
+                 ctrl_group=None, data_group=None, on_arrival=None, on_receive=None, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        if torch.device(device).type != "cuda":
+            raise RuntimeError("PeerShardChannel needs CUDA devices (NVLink peer memory)")
+        self.slot_rows, self.width, self.n_slots = int(slot_rows), int(width), int(n_slots)
+        self.slot_elems = self.slot_rows * self.width
+        self.sym = symm.empty(world * self.n_slots * self.slot_elems, dtype=dtype, device=device)
+        self.hdl = symm.rendezvous(self.sym, group if group is not None else dist.group.WORLD)
+        self.uses = 0            # source: batches packed into peer slots so far
+        self.open = {}           # source: slot -> (first byte address, bytes) of batches not yet sent
+        super().__init__(rank, world, device, dtype, ctrl_group, data_group, on_arrival, on_receive)
+
+    def _offset(self, src: int, slot: int) -> int:
+        return (src * self.n_slots + slot) * self.slot_elems
+
+    def alloc(self, rows: int, width: int):
+        """Source rank: destination for a batch output of ``rows`` x ``width`` (a view of rank 0's
+        memory), or None when it does not fit a slot (the caller packs locally; ``send`` then ships
+        the payload over NCCL)."""
+        if width != self.width or rows > self.slot_rows:
+            return None
+        slot = self.uses % self.n_slots
+        if self.uses >= self.n_slots:  # stream-ordered: rank 0 released this slot's previous batch
+            self.hdl.wait_signal(0, slot, 600000)
+        self.uses += 1
+        view = self.hdl.get_buffer(0, (rows, width), self.dtype, self._offset(self.rank, slot))
+        self.open[slot] = (view.data_ptr(), rows * width * view.element_size())
+        return view
+
+    def send(self, req_id: int, shard_id: int, emb, last: bool = False) -> None:
+        p = emb.data_ptr()
+        slot = next((k for k, (base, n) in self.open.items() if base <= p < base + n), None)
+        if slot is None:
+            return super().send(req_id, shard_id, emb, last)
+        row0 = (p - self.open[slot][0]) // (self.width * emb.element_size())
+        h = self.torch.tensor([req_id, shard_id, emb.shape[0], emb.shape[1], slot, row0, int(last), 0],
+                              dtype=self.torch.int64)
+        self.dist.send(h, 0, group=self._g(self.ctrl, self.rank))
+        if last:
+            del self.open[slot]
+
+    def _peer_arrival(self, src, rid, sid, rows, width, slot, row0, last):
+        base = self._offset(src, slot) + row0 * width
+        buf = self.sym[base:base + rows * width].view(rows, width)
+        if self.on_receive is not None:
+            self.on_receive(rid, sid, buf)
+        extra = self.on_arrival(buf) if self.on_arrival is not None else None
+        if last:  # every row of the slot handed on: release it, stream-ordered after the work above
+            self.hdl.put_signal(src, slot)
+        self.ready.put((rid, sid, buf if extra is None else extra))
 
 
 @dataclass
@@ -280,7 +364,7 @@ class ImagePathService:
             if inflight is not None and inflight[1].query():
                 batch, _, out = inflight
                 t_done = clock()
-                for it in batch:
+                for k, it in enumerate(batch):
                     a, b = out.item_spans[it.seq]
                     rows0 = sum(out.image_tokens[:a])
                     rows1 = rows0 + sum(out.image_tokens[a:b])
@@ -290,7 +374,7 @@ class ImagePathService:
                             y = self.connector(out.embeds[rows0:rows1])
                             self.projected[(it.request_id, it.shard_id)] = tuple(y.shape)
                     else:
-                        channel.send(it.request_id, it.shard_id, out.embeds[rows0:rows1])
+                        channel.send(it.request_id, it.shard_id, out.embeds[rows0:rows1], last=k == len(batch) - 1)
                 inflight = None
                 progressed = True
             if inflight is None and queue:
@@ -300,7 +384,8 @@ class ImagePathService:
                     batch = [queue[i] for i in idx]
                     for i in sorted(idx, reverse=True):
                         queue.pop(i)
-                    out = self.executor.run(batch, img_lists)
+                    out_alloc = getattr(channel, "alloc", None) if self.rank != 0 else None
+                    out = self.executor.run(batch, img_lists, out_alloc=out_alloc)
                     ev = torch.cuda.Event()
                     ev.record()
                     inflight = (batch, ev, out)

@@ -34,6 +34,13 @@ def main():
     ap.add_argument("--ms-per-tile", type=float, default=5.0, help="routing cost model (measured ~4.9 on B200)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--connector", action="store_true", help="apply the LLM-side projector on rank 0 as shards land")
+    ap.add_argument("--handoff", default="peer", choices=["peer", "nccl"],
+                    help="peer: encoders pack straight into rank 0's memory over NVLink (PeerShardChannel); "
+                         "nccl: pack locally + NCCL send")
+    ap.add_argument("--slot-images", type=int, default=16,
+                    help="peer slot size in max-tile images (larger batches fall back to NCCL)")
+    ap.add_argument("--verify", action="store_true",
+                    help="rank 0 re-encodes every remote shard and compares it bit for bit with what arrived")
     ap.add_argument("--watchdog-s", type=float, default=0.0, help="dump all thread stacks after this many seconds")
     args = ap.parse_args()
     if args.watchdog_s > 0:
@@ -44,7 +51,7 @@ def main():
     import torch.distributed as dist
     from paper_2502_00937_b200 import core, policies, workload
     from paper_2502_00937_b200.executor import ImagePathExecutor
-    from paper_2502_00937_b200.service import ImagePathService, ShardChannel
+    from paper_2502_00937_b200.service import ImagePathService, PeerShardChannel, ShardChannel, route_requests
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -79,11 +86,30 @@ def main():
     svc = ImagePathService(spec, ex, rank=rank, world=world, policies=pol, max_batch={"encode": args.max_batch},
                            cost_ms=lambda tiles: args.ms_per_tile * tiles, ttft_slo_ms=2000.0, connector=connector)
     chan = None
+    digests = {}
+
+    def digest(x):
+        v = x.contiguous().view(torch.int16).reshape(-1).long()
+        w = torch.arange(v.numel(), device=v.device) % 65521 + 1
+        return torch.stack([v.sum(), (v * w).sum()])
+
+    def on_receive(rid, sid, buf):  # receiver thread, before the slot is released
+        digests[(rid, sid)] = (digest(buf), tuple(buf.shape))
+
     if world > 1:
         ctrl_g, data_g = ShardChannel.make_groups(world)
         # remote shards are projected by the receiver threads, on their own streams, as they land
-        chan = ShardChannel(rank, world, torch.device("cuda", local), torch.bfloat16, ctrl_group=ctrl_g,
-                            data_group=data_g, on_arrival=connector)
+        kw = dict(ctrl_group=ctrl_g, data_group=data_g, on_arrival=connector,
+                  on_receive=on_receive if args.verify else None)
+        dev = torch.device("cuda", local)
+        if args.handoff == "peer":
+            enc = spec.encoder
+            P1 = (spec.tile_edge_px // enc.patch_px) ** 2 + 1
+            width = enc.hidden * (1 + len(enc.out_layers)) if enc.family == "mllama" else enc.hidden
+            chan = PeerShardChannel(rank, world, dev, torch.bfloat16, slot_rows=args.slot_images * spec.max_tiles_per_image * P1,
+                                    width=width, **kw)
+        else:
+            chan = ShardChannel(rank, world, dev, torch.bfloat16, **kw)
     res = svc.replay(reqs, channel=chan, barrier=(dist.barrier if world > 1 else None))
     if rank == 0:
         s = res.summary()
@@ -94,7 +120,22 @@ def main():
                           "images_per_request": IMAGES_PER_REQUEST, "requests": len(reqs), "images": n_img},
                 "batcher": {"router": "least_pending", "scheduler": args.scheduler, "max_batch_encode": args.max_batch},
                 "connector": "mllama multi_modal_projector on rank 0" if args.connector else None,
+                "handoff": (args.handoff if world > 1 else None),
+                "handoff_shards": (dict(chan.counts) if chan is not None else None),
                 "model": spec.name}
+        if args.verify and world > 1:
+            torch.cuda.synchronize()
+            routes = route_requests(reqs, world, svc.cost_ms, svc.policies)
+            by_id = {r.id: r for r in reqs}
+            from paper_2502_00937_b200.service import synthetic_image
+            bad = 0
+            for (rid, sid), (dg, shape) in sorted(digests.items()):
+                _, idx = routes[rid][sid]
+                r = by_id[rid]
+                imgs = [synthetic_image(rid, i, r.images[i].width_px, r.images[i].height_px) for i in idx]
+                ref = ex.encode_images(imgs).embeds
+                bad += int(tuple(ref.shape) != shape or not torch.equal(digest(ref), dg))
+            line["verify"] = {"remote_shards": len(digests), "mismatches": bad}
         print(json.dumps(line), file=result_out, flush=True)
     if world > 1:
         dist.barrier()

@@ -267,6 +267,8 @@ def test_pack_mllama_layout(mk, n_inter, d):
     out = ops.pack_mllama(fin, inter)
     ref = torch.cat([fin.bfloat16(), torch.stack(list(inter), dim=-1).reshape(rows, -1)], -1)
     assert torch.equal(out, ref)
+    # staged form (peer destinations: rows assembled in shared memory, one bulk copy per row)
+    assert torch.equal(ops.pack_mllama(fin, inter, peer=True), ref)
 
 
 def test_pack_drop_cls(mk):

@@ -1,0 +1,30 @@
+"""Two-GPU handoff (runs only where the box has >= 2 GPUs; the single-GPU suite skips it).
+
+The replay service with the fused pack + NVLink handoff (PeerShardChannel: encoders on rank 1 pack
+straight into rank 0's memory) and with the NCCL payload path; rank 0 re-encodes every remote
+shard and compares it bit for bit with what arrived (replay.py --verify)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("handoff,port", [("peer", 29531), ("nccl", 29532)])
+def test_replay_handoff_bit_exact(handoff, port):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "replay.py"),
+           "--duration-s", "3", "--verify", "--handoff", handoff, "--watchdog-s", "240"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["handoff"] == handoff
+    assert line["verify"]["remote_shards"] > 0 and line["verify"]["mismatches"] == 0, line["verify"]
+    if handoff == "peer":
+        assert line["handoff_shards"]["peer"] > 0
