@@ -7,51 +7,44 @@
 // (DESIGN.md §3), restated op-for-op in oracle/preprocess.py so results are bit-identical:
 // every fp32 operation is an explicit round-to-nearest intrinsic (no FMA contraction).
 //
-// Grid: one CTA per (tile, patch-row).  Each thread produces 8 consecutive bf16 of a patch
-// row and stores them as one 16-byte vector, so the dominant HBM stream (the bf16 patch
-// matrix) is written fully coalesced; the uint8 source is read through L1 (each source pixel
-// is touched by <= 4 neighbouring outputs).
+// Grid: one CTA per (tile, patch-row) band of p pixel rows.  Each thread resamples whole
+// pixels (the bilinear weights are shared by the three channels), writes the normalised bf16
+// values into the band's patch vectors in shared memory, and the band — a contiguous
+// per_side * k_pad run of the patch matrix — leaves with 16-byte stores, a warp covering 512
+// contiguous bytes.  The uint8 source is read through L1 (each source pixel feeds <= 4 outputs
+// per channel when upsampling).
 #include "sm100_common.cuh"
 #include "mmk_internal.h"
 
 namespace mmk {
+
+constexpr int kMaxPatch = 64;  // patch edge limit of the band kernel
+
+// Exact uint8 -> fp32 on the FMA pipe: 2^23 + b has b in its low mantissa bits (the I2F
+// conversion runs on the quarter-rate XU pipe and was this kernel's limiter).
+MMK_DEV float u8_to_f32(uint32_t b) { return __fsub_rn(__uint_as_float(0x4B000000u | b), 8388608.f); }
 
 struct PrepImage {
   int img, slot, tiles, w, h, rows, cols, nw, nh;
   int64_t off;
 };
 
+#ifndef MMK_PREP_MINB
+#define MMK_PREP_MINB 4
+#endif
+#ifndef MMK_PREP_UNROLL
+#define MMK_PREP_UNROLL 2
+#endif
+constexpr int kPrepUnroll = MMK_PREP_UNROLL;  // band rows in flight per thread
 template <bool CHW>
-MMK_DEV float bilinear_u8(const uint8_t* __restrict__ img, int w, int h, int c, float sclx, float scly, int X,
-                          int Y) {
-  float sx = __fsub_rn(__fmul_rn(__fadd_rn(static_cast<float>(X), 0.5f), sclx), 0.5f);
-  float sy = __fsub_rn(__fmul_rn(__fadd_rn(static_cast<float>(Y), 0.5f), scly), 0.5f);
-  sx = fmaxf(sx, 0.f);
-  sy = fmaxf(sy, 0.f);
-  int x0 = static_cast<int>(floorf(sx)), y0 = static_cast<int>(floorf(sy));
-  x0 = min(x0, w - 1);
-  y0 = min(y0, h - 1);
-  const int x1 = min(x0 + 1, w - 1), y1 = min(y0 + 1, h - 1);
-  const float fx = __fsub_rn(sx, static_cast<float>(x0));
-  const float fy = __fsub_rn(sy, static_cast<float>(y0));
-  auto px = [&](int y, int x) -> float {
-    if constexpr (CHW) return img[(static_cast<int64_t>(c) * h + y) * w + x];
-    else return img[(static_cast<int64_t>(y) * w + x) * 3 + c];
-  };
-  const float p00 = px(y0, x0), p01 = px(y0, x1), p10 = px(y1, x0), p11 = px(y1, x1);
-  const float gx = __fsub_rn(1.f, fx), gy = __fsub_rn(1.f, fy);
-  const float top = __fadd_rn(__fmul_rn(gx, p00), __fmul_rn(fx, p01));
-  const float bot = __fadd_rn(__fmul_rn(gx, p10), __fmul_rn(fx, p11));
-  return __fadd_rn(__fmul_rn(gy, top), __fmul_rn(fy, bot));
-}
-
-template <bool CHW>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, MMK_PREP_MINB)
 preprocess_kernel(const uint8_t* __restrict__ src, const int64_t* __restrict__ src_off, const int32_t* __restrict__ w,
                   const int32_t* __restrict__ h, const int64_t* __restrict__ tile_off,
                   const int32_t* __restrict__ geom, int n, int T, int p, int k_pad, int mode, int thumb,
                   const float* __restrict__ scale3, const float* __restrict__ shift3,
                   __nv_bfloat16* __restrict__ patches) {
+  extern __shared__ __align__(16) uint8_t prep_smem[];
+  __nv_bfloat16* band = reinterpret_cast<__nv_bfloat16*>(prep_smem);  // [per_side][k_pad]
   griddep_wait();  // PDL: inputs come from the preceding kernel
   griddep_launch_dependents();
   __shared__ PrepImage meta;
@@ -100,35 +93,103 @@ preprocess_kernel(const uint8_t* __restrict__ src, const int64_t* __restrict__ s
   const float scly = __fdiv_rn(static_cast<float>(m.h), static_cast<float>(rh));
   const int pp = p * p;
   const int kreal = 3 * pp;
-  const int total = per_side * k_pad;  // outputs of this CTA
-  __nv_bfloat16* out = patches + (static_cast<int64_t>(g) * per_side * per_side + static_cast<int64_t>(pr) * per_side) * k_pad;
-  for (int base = threadIdx.x * 8; base < total; base += 256 * 8) {
-    uint32_t packed[4];
-#pragma unroll
-    for (int e = 0; e < 8; e += 2) {
-      float v2[2];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int idx = base + e + u;
-        const int pc = idx / k_pad;      // patch column inside the patch row
-        const int col = idx - pc * k_pad;
-        float val = 0.f;
-        if (col < kreal) {
-          const int c = col / pp;
-          const int rem = col - c * pp;
-          const int iy = rem / p, ix = rem - iy * p;
-          const int X = ox + pc * p + ix;
-          const int Y = oy + pr * p + iy;
-          float v = 0.f;  // padding pixel value (before normalisation), as HF Mllama pads with 0
-          if (is_thumb || crop || (X < m.nw && Y < m.nh)) v = bilinear_u8<CHW>(img, m.w, m.h, c, sclx, scly, X, Y);
-          val = __fadd_rn(__fmul_rn(v, s_scale[c]), s_shift[c]);
-        }
-        v2[u] = val;
-      }
-      packed[e / 2] = pack_bf16x2(v2[0], v2[1]);
-    }
-    st_global_v4(out + base, packed[0], packed[1], packed[2], packed[3]);
+  const float sc0 = s_scale[0], sc1 = s_scale[1], sc2 = s_scale[2];
+  const float sh0 = s_shift[0], sh1 = s_shift[1], sh2 = s_shift[2];
+  // 1) resample the band's p x T pixels.  The row-side bilinear terms depend only on the band
+  //    row: computed once into shared memory.  Each thread owns fixed columns (the column-side
+  //    terms and the patch coordinates are hoisted out of the row loop) and produces all three
+  //    channels of each pixel; a warp covers 32 consecutive columns of one row.
+  __shared__ int64_t s_r0[kMaxPatch], s_r1[kMaxPatch];  // byte offsets of source rows y0, y1
+  __shared__ float s_fy[kMaxPatch], s_gy[kMaxPatch];
+  if (threadIdx.x < p) {
+    const int Y = oy + pr * p + threadIdx.x;
+    float sy = __fsub_rn(__fmul_rn(__fadd_rn(static_cast<float>(Y), 0.5f), scly), 0.5f);
+    sy = fmaxf(sy, 0.f);
+    int y0 = static_cast<int>(floorf(sy));
+    y0 = min(y0, m.h - 1);
+    const int y1 = min(y0 + 1, m.h - 1);
+    const float fy = __fsub_rn(sy, static_cast<float>(y0));
+    const int64_t row_bytes = CHW ? m.w : 3ll * m.w;
+    s_r0[threadIdx.x] = y0 * row_bytes;
+    s_r1[threadIdx.x] = y1 * row_bytes;
+    s_fy[threadIdx.x] = fy;
+    s_gy[threadIdx.x] = __fsub_rn(1.f, fy);
   }
+  __syncthreads();
+  const int64_t plane = CHW ? static_cast<int64_t>(m.h) * m.w : 1;  // channel stride
+#ifndef MMK_PREP_NO_PREFETCH
+  {  // pull the band's source rows into L2 up front (bulk prefetch), so the per-pixel byte loads
+     // below hit L2 instead of each waiting on HBM
+    const auto col_of = [&](int X) {
+      float sx = __fsub_rn(__fmul_rn(__fadd_rn(static_cast<float>(X), 0.5f), sclx), 0.5f);
+      return min(static_cast<int>(floorf(fmaxf(sx, 0.f))), m.w - 1);
+    };
+    const int xa = col_of(ox), xb = min(col_of(ox + T - 1) + 1, m.w - 1);
+    const int64_t rb = CHW ? m.w : 3ll * m.w;
+    const int ya = static_cast<int>(s_r0[0] / rb), yb = static_cast<int>(s_r1[p - 1] / rb);
+    const int nrows = (yb - ya + 1) * (CHW ? 3 : 1);
+    for (int r = threadIdx.x; r < nrows; r += blockDim.x) {
+      const int c = CHW ? r / (yb - ya + 1) : 0;
+      const int y = ya + r - c * (yb - ya + 1);
+      const uint8_t* lo = img + c * plane + y * rb + (CHW ? xa : 3 * xa);
+      const uint8_t* hi = img + c * plane + y * rb + (CHW ? xb + 1 : 3 * (xb + 1));
+      const uintptr_t a0 = reinterpret_cast<uintptr_t>(lo) & ~uintptr_t(15);
+      const uintptr_t end = reinterpret_cast<uintptr_t>(img + 3ll * m.w * m.h) & ~uintptr_t(15);  // stay inside
+      const uintptr_t a1 = min((reinterpret_cast<uintptr_t>(hi) + 15) & ~uintptr_t(15), end);
+      if (a1 > a0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(static_cast<uint32_t>(a1 - a0)) : "memory");
+    }
+  }
+#endif
+  const int row_lim = (is_thumb || crop) ? p : min(p, m.nh - (oy + pr * p));  // rows inside the resized image
+  for (int xl = threadIdx.x; xl < T; xl += blockDim.x) {
+    const int pc = xl / p, ix = xl - pc * p;
+    const int X = ox + xl;
+    const bool col_in = is_thumb || crop || X < m.nw;
+    // same operation sequence as the oracle's bilinear sample (bit-identical), column side
+    float sx = __fsub_rn(__fmul_rn(__fadd_rn(static_cast<float>(X), 0.5f), sclx), 0.5f);
+    sx = fmaxf(sx, 0.f);
+    int x0 = static_cast<int>(floorf(sx));
+    x0 = min(x0, m.w - 1);
+    const int x1 = min(x0 + 1, m.w - 1);
+    const float fx = __fsub_rn(sx, static_cast<float>(x0));
+    const float gx = __fsub_rn(1.f, fx);
+    const int cx0 = CHW ? x0 : 3 * x0, cx1 = CHW ? x1 : 3 * x1;  // byte offsets inside a row
+    __nv_bfloat16* o = band + pc * k_pad + ix;  // patch vector order (c, py, px)
+#pragma unroll kPrepUnroll
+    for (int iy = 0; iy < p; ++iy, o += p) {
+      float v[3] = {0.f, 0.f, 0.f};  // padding pixel value (before normalisation): 0, as HF Mllama
+      if (col_in && iy < row_lim) {
+        const uint8_t* a = img + s_r0[iy];
+        const uint8_t* b = img + s_r1[iy];
+        const float fy = s_fy[iy], gy = s_gy[iy];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const int64_t co = c * plane;
+          const float p00 = u8_to_f32(__ldg(a + co + cx0)), p01 = u8_to_f32(__ldg(a + co + cx1));
+          const float p10 = u8_to_f32(__ldg(b + co + cx0)), p11 = u8_to_f32(__ldg(b + co + cx1));
+          const float top = __fadd_rn(__fmul_rn(gx, p00), __fmul_rn(fx, p01));
+          const float bot = __fadd_rn(__fmul_rn(gx, p10), __fmul_rn(fx, p11));
+          v[c] = __fadd_rn(__fmul_rn(gy, top), __fmul_rn(fy, bot));
+        }
+      }
+      o[0] = __float2bfloat16_rn(__fadd_rn(__fmul_rn(v[0], sc0), sh0));
+      o[pp] = __float2bfloat16_rn(__fadd_rn(__fmul_rn(v[1], sc1), sh1));
+      o[2 * pp] = __float2bfloat16_rn(__fadd_rn(__fmul_rn(v[2], sc2), sh2));
+    }
+  }
+  // 2) zero the K padding of every patch vector
+  const int padw = k_pad - kreal;
+  for (int q = threadIdx.x; q < per_side * padw; q += blockDim.x) {
+    const int pc = q / padw;
+    band[pc * k_pad + kreal + (q - pc * padw)] = __float2bfloat16_rn(0.f);
+  }
+  __syncthreads();
+  // 3) the band is one contiguous run of the patch matrix: stream it out
+  const uint4* sv = reinterpret_cast<const uint4*>(band);
+  uint4* dv = reinterpret_cast<uint4*>(patches + (static_cast<int64_t>(g) * per_side + pr) * per_side * k_pad);
+  const int nvec = per_side * k_pad / 8;
+  for (int i = threadIdx.x; i < nvec; i += blockDim.x) dv[i] = sv[i];
 }
 
 }  // namespace mmk
@@ -142,19 +203,25 @@ extern "C" int mmk_preprocess(const uint8_t* src, const int64_t* src_off, int32_
                               const float* scale3, const float* shift3, void* patches, cudaStream_t stream) {
   if (n < 0 || total_tiles < 0) return set_error(MMK_ERR_ARG, "preprocess: negative sizes");
   if (patch_px < 1 || tile_px % patch_px != 0) return set_error(MMK_ERR_ARG, "preprocess: tile_px %% patch_px != 0");
+  if (patch_px > kMaxPatch) return set_error(MMK_ERR_UNSUPPORTED, "preprocess: patch_px %d > %d", patch_px, kMaxPatch);
   if (k_pad < 3 * patch_px * patch_px || k_pad % 8 != 0) return set_error(MMK_ERR_ARG, "preprocess: bad k_pad");
   if (mode != 0 && mode != 1) return set_error(MMK_ERR_ARG, "preprocess: mode must be 0 or 1");
   if (reinterpret_cast<uintptr_t>(patches) & 15) return set_error(MMK_ERR_ARG, "preprocess: patches not 16B aligned");
   if (n == 0 || total_tiles == 0) return MMK_OK;
   const int blocks = total_tiles * (tile_px / patch_px);
-  if (src_chw)
-    (void)launch_kernel(preprocess_kernel<true>, dim3(blocks), dim3(256), 0, stream, 1, total_tiles <= 64, src, src_off, w, h, tile_off, geom, n, tile_px, patch_px, k_pad,
-                                                        mode, thumbnail, scale3, shift3,
-                                                        reinterpret_cast<__nv_bfloat16*>(patches));
-  else
-    (void)launch_kernel(preprocess_kernel<false>, dim3(blocks), dim3(256), 0, stream, 1, total_tiles <= 64, src, src_off, w, h, tile_off, geom, n, tile_px, patch_px,
-                                                         k_pad, mode, thumbnail, scale3, shift3,
-                                                         reinterpret_cast<__nv_bfloat16*>(patches));
+  const int smem = (tile_px / patch_px) * k_pad * 2;
+  if (smem > 200 * 1024) return set_error(MMK_ERR_UNSUPPORTED, "preprocess: patch row band of %d bytes", smem);
+  auto* out = reinterpret_cast<__nv_bfloat16*>(patches);
+  auto go = [&](auto kern) -> cudaError_t {
+    if (smem > 48 * 1024) {
+      const cudaError_t a = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (a != cudaSuccess) return a;
+    }
+    return launch_kernel(kern, dim3(blocks), dim3(256), smem, stream, 1, total_tiles <= 64, src, src_off, w, h,
+                         tile_off, geom, n, tile_px, patch_px, k_pad, mode, thumbnail, scale3, shift3, out);
+  };
+  const cudaError_t le = src_chw ? go(preprocess_kernel<true>) : go(preprocess_kernel<false>);
+  if (le != cudaSuccess) return set_cuda_error(le, "preprocess: launch");
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "preprocess: launch");
 }

@@ -16,11 +16,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.gpu
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-@pytest.mark.parametrize("handoff,port", [("peer", 29531), ("nccl", 29532)])
-def test_replay_handoff_bit_exact(handoff, port):
+@pytest.mark.parametrize("handoff,port,model", [("peer", 29531, "llama3.2-11b"), ("nccl", 29532, "llama3.2-11b"),
+                                                ("peer", 29533, "llava-clip-l14-336")])
+def test_replay_handoff_bit_exact(handoff, port, model):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "replay.py"),
-           "--duration-s", "3", "--verify", "--handoff", handoff, "--watchdog-s", "240"]
+           "--duration-s", "3", "--verify", "--handoff", handoff, "--model", model, "--watchdog-s", "240"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
