@@ -565,6 +565,48 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
           }
           __syncwarp();
         }
+      } else if constexpr (EPI == MMK_EPI_F32) {
+        // fp32 output (patch embedding) through the same two 32x32 fp32 slots: rows staged
+        // 128B-swizzled, TMA-stored (rows >= M clipped by the map) — a thread-per-row float4
+        // store would scatter every warp store over 32 rows
+#pragma unroll 1
+        for (int c = 0; c < kColsPerWarp / 32; ++c) {
+          const int col_in_tile = half * kColsPerWarp + c * 32;
+          const int col = n0 + col_in_tile;
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tm_row + col_in_tile, r);
+          tmem_ld_wait();
+          if (c == kColsPerWarp / 32 - 1) {  // accumulator fully read: release it early
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
+          }
+          const int slot = c & 1;
+          if (lane == 0) tma_store_wait_read<1>();  // the store that last used this slot has read it
+          __syncwarp();
+          uint8_t* rowp = ebuf + slot * 4096 + lane * 128;
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+          if (bias != nullptr) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + col + i));
+              v[i] += b4.x; v[i + 1] += b4.y; v[i + 2] += b4.z; v[i + 3] += b4.w;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(rowp + ((j ^ (lane & 7)) << 4)) =
+                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmap_out, ebuf + slot * 4096, col, m0 + static_cast<int>(q) * 32);
+            tma_store_commit();
+          }
+          __syncwarp();
+        }
       } else {
         const int row = m0 + q * 32 + lane;
         const bool row_ok = row < M;
@@ -583,7 +625,7 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
         if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
       }
     }
-    if constexpr (kTmaStore || RES_TMA) {
+    if constexpr (kTmaStore || RES_TMA || EPI == MMK_EPI_F32) {
       if (lane == 0) tma_store_wait<0>();
       __syncwarp();
     }
@@ -696,7 +738,7 @@ extern "C" int mmk_gemm_bf16(const void* a, int64_t lda, const void* b, int64_t 
     if (!f32_out) {
       rc = make_tmap_2d_bf16(&to, out, n, m, ldo, 64, 32, true);
       if (rc) return rc;
-    } else if (epilogue == MMK_EPI_RESID_F32) {
+    } else {  // fp32 output / residual: [32 rows][32 cols] boxes
       const uint64_t dims[2] = {static_cast<uint64_t>(n), static_cast<uint64_t>(m)};
       const uint64_t strides[1] = {static_cast<uint64_t>(ldo) * 4};
       const uint32_t box[2] = {32, 32};

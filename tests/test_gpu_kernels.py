@@ -132,7 +132,7 @@ def test_preprocess_thumbnail_spec_bit_exact(mk):
 
 # ----------------------------------------------------------------------------- GEMM
 @pytest.mark.parametrize("m,n,k", [(1, 256, 64), (129, 768, 592), (1576, 2304, 768), (5000, 3840, 1280),
-                                   (3000, 1280, 5120), (700, 1024, 4096)])
+                                   (3000, 1280, 5120), (700, 1024, 4096), (20011, 1280, 640)])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3, 4])
 def test_gemm_epilogues(mk, m, n, k, epi):
     _, ops, _ = mk
