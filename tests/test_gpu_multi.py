@@ -16,12 +16,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.mark.gpu
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-@pytest.mark.parametrize("handoff,port,model", [("peer", 29531, "llama3.2-11b"), ("nccl", 29532, "llama3.2-11b"),
-                                                ("peer", 29533, "llava-clip-l14-336")])
-def test_replay_handoff_bit_exact(handoff, port, model):
+@pytest.mark.parametrize("handoff,port,model,slot_images", [
+    ("peer", 29531, "llama3.2-11b", 16), ("nccl", 29532, "llama3.2-11b", 16),
+    ("peer", 29533, "llava-clip-l14-336", 16),
+    ("peer", 29534, "llama3.2-11b", 1)])  # one-image slots: most batches take the NCCL fallback
+def test_replay_handoff_bit_exact(handoff, port, model, slot_images):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "replay.py"),
-           "--duration-s", "3", "--verify", "--handoff", handoff, "--model", model, "--watchdog-s", "240"]
+           "--duration-s", "3", "--verify", "--handoff", handoff, "--model", model, "--slot-images", str(slot_images), "--watchdog-s", "240"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
@@ -29,3 +31,5 @@ def test_replay_handoff_bit_exact(handoff, port, model):
     assert line["verify"]["remote_shards"] > 0 and line["verify"]["mismatches"] == 0, line["verify"]
     if handoff == "peer":
         assert line["handoff_shards"]["peer"] > 0
+    if slot_images == 1:
+        assert line["handoff_shards"]["nccl"] > 0
