@@ -911,7 +911,11 @@ int launch_attn_tc(const void* qkv, void* out, const int32_t* cu, int n_seq, int
     const char* e = getenv("MMK_ATTN_SPEC");
     return e ? atoi(e) != 0 : true;
   }();
-  constexpr int BKV = HD == 64 ? 64 : 112, NQ = HD == 64 ? 3 : 2;
+#ifndef MMK_ATTN_HD80_BKV
+#define MMK_ATTN_HD80_BKV 112
+#define MMK_ATTN_HD80_NQ 2
+#endif
+  constexpr int BKV = HD == 64 ? 64 : MMK_ATTN_HD80_BKV, NQ = HD == 64 ? 3 : MMK_ATTN_HD80_NQ;
   const int64_t items = static_cast<int64_t>((max_s + NQ * kTcBQ - 1) / (NQ * kTcBQ)) * heads * n_seq;
   const bool persist = force == 1 || (force != 0 && items > 2 * num_sms());
   if (persist) {
