@@ -65,8 +65,12 @@ struct TcAttnCfg {
   static constexpr int kSmem = kBarOff + 256 + 1024;
   static constexpr int kThreads = 32 * (5 * NQ + 1);  // NQ softmax warpgroups, TMA warp, NQ MMA warps
   static constexpr int kOBase = NQ * BKV;                    // TMEM column of O_0 (O_t: + t*HD)
-  static constexpr int kPBase = (kOBase + NQ * HD + 31) / 32 * 32;  // P_t (bf16 pairs): + t*kPStride
-  static constexpr int kPStride = (BKV / 2 + 31) / 32 * 32;
+  // P_t (bf16 pairs) in its own columns when S + O + P fit 512, else aliased onto S_t (then S_t(j+1)
+  // is issued only after PV_t(j) has retired, instead of as soon as S_t(j) is in registers)
+  static constexpr int kPStrideSep = (BKV / 2 + 31) / 32 * 32;
+  static constexpr bool kAlias = (kOBase + NQ * HD + 31) / 32 * 32 + (NQ - 1) * kPStrideSep + BKV / 2 > 512;
+  static constexpr int kPBase = kAlias ? 0 : (kOBase + NQ * HD + 31) / 32 * 32;  // P_t: + t*kPStride
+  static constexpr int kPStride = kAlias ? BKV : kPStrideSep;
   static_assert(kPBase + (NQ - 1) * kPStride + BKV / 2 <= 512, "TMEM overflow: S + O + P > 512 columns");
   static_assert(BKV % 16 == 0, "key tile");
   static_assert(kSmem <= 232448, "shared memory overflow");
@@ -442,22 +446,26 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
       // gaps are filled by the other's MUFU work (attention +2 % in-step, r01_attention.md).
       if (t > 0 && nkv > 1) mbar_wait(&p_full[0], 0);
       tc_fence_after();
-      for (int j = 0; j <= nkv; ++j) {
+      auto do_s = [&](int j) {
         const int st = j % C::STAGES;
-        const int pst = (j - 1 + C::STAGES) % C::STAGES;
-        if (j < nkv) {
-          mbar_wait(&k_full[st], (j / C::STAGES) & 1);
-          if (j > 0) mbar_wait(&s_free[t], (j - 1) & 1);  // softmax has S_t(j-1) in registers
-          tc_fence_after();
-          if (t < 2) { TR(2, j, 0) }
-          const uint32_t k_addr = smem_u32(tile_ptr(C::kKVOff + st * C::kStageBytes));
-          if (elect_one()) {
-            issue_s<HD, BKV, NQ>(s_tm, q_addr, k_addr);
-            umma_commit(&s_full[t]);
-          }
-          __syncwarp();
-          if (t < 2) { TR(2, j, 1 + t) }
+        mbar_wait(&k_full[st], (j / C::STAGES) & 1);
+        if (j > 0) {
+          if constexpr (C::kAlias) mbar_wait(&pv_done[t], (j - 1) & 1);  // PV_t(j-1) has read P_t = S_t
+          else mbar_wait(&s_free[t], (j - 1) & 1);                        // softmax has S_t(j-1) in registers
         }
+        tc_fence_after();
+        if (t < 2) { TR(2, j, 0) }
+        const uint32_t k_addr = smem_u32(tile_ptr(C::kKVOff + st * C::kStageBytes));
+        if (elect_one()) {
+          issue_s<HD, BKV, NQ>(s_tm, q_addr, k_addr);
+          umma_commit(&s_full[t]);
+        }
+        __syncwarp();
+        if (t < 2) { TR(2, j, 1 + t) }
+      };
+      for (int j = 0; j <= nkv; ++j) {
+        const int pst = (j - 1 + C::STAGES) % C::STAGES;
+        if (!C::kAlias && j < nkv) do_s(j);
         if (j > 0) {
           mbar_wait(&v_full[pst], ((j - 1) / C::STAGES) & 1);
           mbar_wait(&p_full[t], (j - 1) & 1);
@@ -472,6 +480,7 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
           __syncwarp();
           if (t < 2) { TR(2, j - 1, 5 + t) }
         }
+        if (C::kAlias && j < nkv) do_s(j);
       }
     }
   } else {
@@ -756,21 +765,25 @@ attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       // staggered start (as in attn_fwd_tc): the offset set on the first item persists
       if (t > 0 && oi == 0 && it.nkv > 1) mbar_wait(&p_full[0], 0);
       tc_fence_after();
-      for (int j = 0; j <= it.nkv; ++j) {
-        if (j < it.nkv) {
-          const uint32_t kvj = kv + j;
-          const int st = kvj % C::STAGES;
-          mbar_wait(&k_full[st], (kvj / C::STAGES) & 1);
-          if (g + j > 0) mbar_wait(&s_free[t], (g + j - 1) & 1);
-          tc_fence_after();
-          const uint32_t k_addr = smem_u32(tile_ptr(Lay::kKVOff + st * C::kStageBytes));
-          if (elect_one()) {
-            issue_s<HD, BKV, NQ>(s_tm, q_addr, k_addr);
-            umma_commit(&s_full[t]);
-            if (j == it.nkv - 1) umma_commit(&q_empty[qs]);  // last read of this item's Q
-          }
-          __syncwarp();
+      auto do_s = [&](int j) {
+        const uint32_t kvj = kv + j;
+        const int st = kvj % C::STAGES;
+        mbar_wait(&k_full[st], (kvj / C::STAGES) & 1);
+        if (g + j > 0) {
+          if constexpr (C::kAlias) mbar_wait(&pv_done[t], (g + j - 1) & 1);  // PV_t has read P_t = S_t
+          else mbar_wait(&s_free[t], (g + j - 1) & 1);
         }
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(tile_ptr(Lay::kKVOff + st * C::kStageBytes));
+        if (elect_one()) {
+          issue_s<HD, BKV, NQ>(s_tm, q_addr, k_addr);
+          umma_commit(&s_full[t]);
+          if (j == it.nkv - 1) umma_commit(&q_empty[qs]);  // last read of this item's Q
+        }
+        __syncwarp();
+      };
+      for (int j = 0; j <= it.nkv; ++j) {
+        if (!C::kAlias && j < it.nkv) do_s(j);
         if (j > 0) {
           const uint32_t kvp = kv + j - 1;
           const int pst = kvp % C::STAGES;
@@ -786,6 +799,7 @@ attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_co
           }
           __syncwarp();
         }
+        if (C::kAlias && j < it.nkv) do_s(j);
       }
       kv += it.nkv;
       g += it.nkv;
