@@ -30,19 +30,19 @@ struct PrepImage {
 };
 
 #ifndef MMK_PREP_MINB
-#define MMK_PREP_MINB 4
+#define MMK_PREP_MINB 2
 #endif
 #ifndef MMK_PREP_UNROLL
 #define MMK_PREP_UNROLL 2
 #endif
 constexpr int kPrepUnroll = MMK_PREP_UNROLL;  // band rows in flight per thread
 template <bool CHW>
-__global__ void __launch_bounds__(256, MMK_PREP_MINB)
+__global__ void __launch_bounds__(512, MMK_PREP_MINB)
 preprocess_kernel(const uint8_t* __restrict__ src, const int64_t* __restrict__ src_off, const int32_t* __restrict__ w,
                   const int32_t* __restrict__ h, const int64_t* __restrict__ tile_off,
                   const int32_t* __restrict__ geom, int n, int T, int p, int k_pad, int mode, int thumb,
                   const float* __restrict__ scale3, const float* __restrict__ shift3,
-                  __nv_bfloat16* __restrict__ patches) {
+                  __nv_bfloat16* __restrict__ patches, int parts) {
   extern __shared__ __align__(16) uint8_t prep_smem[];
   __nv_bfloat16* band = reinterpret_cast<__nv_bfloat16*>(prep_smem);  // [per_side][k_pad]
   griddep_wait();  // PDL: inputs come from the preceding kernel
@@ -142,54 +142,61 @@ preprocess_kernel(const uint8_t* __restrict__ src, const int64_t* __restrict__ s
   }
 #endif
   const int row_lim = (is_thumb || crop) ? p : min(p, m.nh - (oy + pr * p));  // rows inside the resized image
-  for (int xl = threadIdx.x; xl < T; xl += blockDim.x) {
-    const int pc = xl / p, ix = xl - pc * p;
-    const int X = ox + xl;
-    const bool col_in = is_thumb || crop || X < m.nw;
-    // same operation sequence as the oracle's bilinear sample (bit-identical), column side
-    float sx = __fsub_rn(__fmul_rn(__fadd_rn(static_cast<float>(X), 0.5f), sclx), 0.5f);
-    sx = fmaxf(sx, 0.f);
-    int x0 = static_cast<int>(floorf(sx));
-    x0 = min(x0, m.w - 1);
-    const int x1 = min(x0 + 1, m.w - 1);
-    const float fx = __fsub_rn(sx, static_cast<float>(x0));
-    const float gx = __fsub_rn(1.f, fx);
-    const int cx0 = CHW ? x0 : 3 * x0, cx1 = CHW ? x1 : 3 * x1;  // byte offsets inside a row
-    __nv_bfloat16* o = band + pc * k_pad + ix;  // patch vector order (c, py, px)
+  // the band is processed in `parts` column ranges of whole patches, sized so that one thread per
+  // column covers a part in one pass (blockDim = the part's columns rounded up to a warp)
+  const int pc_per = (per_side + parts - 1) / parts;
+  for (int pc0 = 0; pc0 < per_side; pc0 += pc_per) {
+    const int pc1 = min(per_side, pc0 + pc_per);
+    if (pc0 > 0) __syncthreads();  // the previous part's copy-out has read the buffer
+    for (int xl = pc0 * p + threadIdx.x; xl < pc1 * p; xl += blockDim.x) {
+      const int pc = xl / p, ix = xl - pc * p;
+      const int X = ox + xl;
+      const bool col_in = is_thumb || crop || X < m.nw;
+      // same operation sequence as the oracle's bilinear sample (bit-identical), column side
+      float sx = __fsub_rn(__fmul_rn(__fadd_rn(static_cast<float>(X), 0.5f), sclx), 0.5f);
+      sx = fmaxf(sx, 0.f);
+      int x0 = static_cast<int>(floorf(sx));
+      x0 = min(x0, m.w - 1);
+      const int x1 = min(x0 + 1, m.w - 1);
+      const float fx = __fsub_rn(sx, static_cast<float>(x0));
+      const float gx = __fsub_rn(1.f, fx);
+      const int cx0 = CHW ? x0 : 3 * x0, cx1 = CHW ? x1 : 3 * x1;  // byte offsets inside a row
+      __nv_bfloat16* o = band + (pc - pc0) * k_pad + ix;  // patch vector order (c, py, px)
 #pragma unroll kPrepUnroll
-    for (int iy = 0; iy < p; ++iy, o += p) {
-      float v[3] = {0.f, 0.f, 0.f};  // padding pixel value (before normalisation): 0, as HF Mllama
-      if (col_in && iy < row_lim) {
-        const uint8_t* a = img + s_r0[iy];
-        const uint8_t* b = img + s_r1[iy];
-        const float fy = s_fy[iy], gy = s_gy[iy];
+      for (int iy = 0; iy < p; ++iy, o += p) {
+        float v[3] = {0.f, 0.f, 0.f};  // padding pixel value (before normalisation): 0, as HF Mllama
+        if (col_in && iy < row_lim) {
+          const uint8_t* a = img + s_r0[iy];
+          const uint8_t* b = img + s_r1[iy];
+          const float fy = s_fy[iy], gy = s_gy[iy];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const int64_t co = c * plane;
-          const float p00 = u8_to_f32(__ldg(a + co + cx0)), p01 = u8_to_f32(__ldg(a + co + cx1));
-          const float p10 = u8_to_f32(__ldg(b + co + cx0)), p11 = u8_to_f32(__ldg(b + co + cx1));
-          const float top = __fadd_rn(__fmul_rn(gx, p00), __fmul_rn(fx, p01));
-          const float bot = __fadd_rn(__fmul_rn(gx, p10), __fmul_rn(fx, p11));
-          v[c] = __fadd_rn(__fmul_rn(gy, top), __fmul_rn(fy, bot));
+          for (int c = 0; c < 3; ++c) {
+            const int64_t co = c * plane;
+            const float p00 = u8_to_f32(__ldg(a + co + cx0)), p01 = u8_to_f32(__ldg(a + co + cx1));
+            const float p10 = u8_to_f32(__ldg(b + co + cx0)), p11 = u8_to_f32(__ldg(b + co + cx1));
+            const float top = __fadd_rn(__fmul_rn(gx, p00), __fmul_rn(fx, p01));
+            const float bot = __fadd_rn(__fmul_rn(gx, p10), __fmul_rn(fx, p11));
+            v[c] = __fadd_rn(__fmul_rn(gy, top), __fmul_rn(fy, bot));
+          }
         }
+        o[0] = __float2bfloat16_rn(__fadd_rn(__fmul_rn(v[0], sc0), sh0));
+        o[pp] = __float2bfloat16_rn(__fadd_rn(__fmul_rn(v[1], sc1), sh1));
+        o[2 * pp] = __float2bfloat16_rn(__fadd_rn(__fmul_rn(v[2], sc2), sh2));
       }
-      o[0] = __float2bfloat16_rn(__fadd_rn(__fmul_rn(v[0], sc0), sh0));
-      o[pp] = __float2bfloat16_rn(__fadd_rn(__fmul_rn(v[1], sc1), sh1));
-      o[2 * pp] = __float2bfloat16_rn(__fadd_rn(__fmul_rn(v[2], sc2), sh2));
     }
+    // 2) zero the K padding of every patch vector of the part
+    const int padw = k_pad - kreal;
+    for (int q = threadIdx.x; q < (pc1 - pc0) * padw; q += blockDim.x) {
+      const int pc = q / padw;
+      band[pc * k_pad + kreal + (q - pc * padw)] = __float2bfloat16_rn(0.f);
+    }
+    __syncthreads();
+    // 3) the part is one contiguous run of the patch matrix: stream it out
+    const uint4* sv = reinterpret_cast<const uint4*>(band);
+    uint4* dv = reinterpret_cast<uint4*>(patches + ((static_cast<int64_t>(g) * per_side + pr) * per_side + pc0) * k_pad);
+    const int nvec = (pc1 - pc0) * k_pad / 8;
+    for (int i = threadIdx.x; i < nvec; i += blockDim.x) dv[i] = sv[i];
   }
-  // 2) zero the K padding of every patch vector
-  const int padw = k_pad - kreal;
-  for (int q = threadIdx.x; q < per_side * padw; q += blockDim.x) {
-    const int pc = q / padw;
-    band[pc * k_pad + kreal + (q - pc * padw)] = __float2bfloat16_rn(0.f);
-  }
-  __syncthreads();
-  // 3) the band is one contiguous run of the patch matrix: stream it out
-  const uint4* sv = reinterpret_cast<const uint4*>(band);
-  uint4* dv = reinterpret_cast<uint4*>(patches + (static_cast<int64_t>(g) * per_side + pr) * per_side * k_pad);
-  const int nvec = per_side * k_pad / 8;
-  for (int i = threadIdx.x; i < nvec; i += blockDim.x) dv[i] = sv[i];
 }
 
 }  // namespace mmk
@@ -209,7 +216,12 @@ extern "C" int mmk_preprocess(const uint8_t* src, const int64_t* src_off, int32_
   if (reinterpret_cast<uintptr_t>(patches) & 15) return set_error(MMK_ERR_ARG, "preprocess: patches not 16B aligned");
   if (n == 0 || total_tiles == 0) return MMK_OK;
   const int blocks = total_tiles * (tile_px / patch_px);
-  const int smem = (tile_px / patch_px) * k_pad * 2;
+  const int per_side = tile_px / patch_px;
+  int parts = 1;  // column parts per band: one thread per column of a part, at most 512 threads
+  while ((per_side + parts - 1) / parts * patch_px > 512) ++parts;
+  const int cols = (per_side + parts - 1) / parts * patch_px;
+  const int threads = (cols + 31) / 32 * 32;
+  const int smem = (per_side + parts - 1) / parts * k_pad * 2;
   if (smem > 200 * 1024) return set_error(MMK_ERR_UNSUPPORTED, "preprocess: patch row band of %d bytes", smem);
   auto* out = reinterpret_cast<__nv_bfloat16*>(patches);
   auto go = [&](auto kern) -> cudaError_t {
@@ -217,8 +229,8 @@ extern "C" int mmk_preprocess(const uint8_t* src, const int64_t* src_off, int32_
       const cudaError_t a = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (a != cudaSuccess) return a;
     }
-    return launch_kernel(kern, dim3(blocks), dim3(256), smem, stream, 1, total_tiles <= 64, src, src_off, w, h,
-                         tile_off, geom, n, tile_px, patch_px, k_pad, mode, thumbnail, scale3, shift3, out);
+    return launch_kernel(kern, dim3(blocks), dim3(threads), smem, stream, 1, total_tiles <= 64, src, src_off, w, h,
+                         tile_off, geom, n, tile_px, patch_px, k_pad, mode, thumbnail, scale3, shift3, out, parts);
   };
   const cudaError_t le = src_chw ? go(preprocess_kernel<true>) : go(preprocess_kernel<false>);
   if (le != cudaSuccess) return set_cuda_error(le, "preprocess: launch");
