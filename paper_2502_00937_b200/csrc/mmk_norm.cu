@@ -85,8 +85,11 @@ layernorm_kernel(const float* __restrict__ x, void* y, int y_f32, int rows, int 
   store_row<VEC>(y, y_f32, row, d, v, lane);
 }
 
+#ifndef MMK_EMBED_MINB
+#define MMK_EMBED_MINB 4  // 64 registers: 4 CTAs per SM (the unbounded 134-register build ran 1 CTA per SM, 2.9x slower)
+#endif
 template <int VEC>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, MMK_EMBED_MINB)
 embed_kernel(const float* __restrict__ patch_out, const int32_t* __restrict__ tile_image,
              const int32_t* __restrict__ tile_slot, const int32_t* __restrict__ image_ar, int total_tiles, int P, int d,
              const float* __restrict__ cls, const float* __restrict__ pos, float pos_scale,

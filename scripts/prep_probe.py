@@ -37,6 +37,27 @@ def main():
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / reps
+    if os.environ.get("EMBED_PROBE"):  # the embedding-assembly kernel on the same batch
+        P = (spec.tile_edge_px // spec.encoder.patch_px) ** 2
+        T = sum(tiles)
+        po = torch.randn(T * P, spec.encoder.hidden, device="cuda")
+        ti, ts = ops.tile_index(plan["tile_off"], n, T)
+
+        def emb():
+            return ops.embed_tokens(po, T, P, enc.cls, enc.pos, enc.pos_scale, *enc.pre_ln, spec.encoder.norm_eps,
+                                    tile_image=ti, tile_slot=ts, image_ar=plan["ar_id"], tile_pos=enc.tile_pos,
+                                    tile_pos_scale=enc.tile_pos_scale, pre_tile=enc.pre_tile,
+                                    pre_scale=enc.pre_scale, slots=enc.slots)
+        r = emb()
+        for _ in range(3):
+            emb()
+        s.record()
+        for _ in range(reps):
+            emb()
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / reps
+        print(f"embed {T} tiles: {ms * 1e3:.1f} us, {(po.numel() + r.numel()) * 4 / ms / 1e6:.0f} GB/s (patch in + resid out)")
     nbytes = b.src.numel() + out.numel() * 2
     print(f"{os.environ.get('MMK_LIB', 'libmmk.so')}: {model} {n} images {sum(tiles)} tiles: {ms * 1e3:.1f} us, "
           f"{nbytes / ms / 1e6:.0f} GB/s (src {b.src.numel() / 1e6:.1f} MB + patches {out.numel() * 2 / 1e6:.1f} MB)")
