@@ -37,6 +37,19 @@ def main():
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / reps
+    if os.environ.get("LN_PROBE"):  # K3 LayerNorm at the bench step's residual shape
+        x = torch.randn(120075, spec.encoder.hidden, device="cuda")
+        gw, gb = torch.randn(spec.encoder.hidden, device="cuda"), torch.randn(spec.encoder.hidden, device="cuda")
+        y = torch.empty(x.shape, dtype=torch.bfloat16, device="cuda")
+        for _ in range(3):
+            ops.layernorm(x, gw, gb, 1e-5, out=y)
+        s.record()
+        for _ in range(reps):
+            ops.layernorm(x, gw, gb, 1e-5, out=y)
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / reps
+        print(f"layernorm 120075 x {x.shape[1]}: {ms * 1e3:.1f} us, {(x.numel() * 6) / ms / 1e6:.0f} GB/s")
     if os.environ.get("EMBED_PROBE"):  # the embedding-assembly kernel on the same batch
         P = (spec.tile_edge_px // spec.encoder.patch_px) ** 2
         T = sum(tiles)
