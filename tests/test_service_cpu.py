@@ -84,3 +84,52 @@ def test_shard_channel_gloo_world2():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert got == [((101, 1), (5, 4), 1.0), ((102, 2), (10, 4), 2.0), ((103, 3), (15, 4), 3.0)]
+
+
+class _SlotRecordingChannel(ShardChannel):
+    """CPU stand-in for PeerShardChannel's header protocol: a header naming a slot carries no
+    payload and is handed to ``_peer_arrival`` (the CUDA class maps it onto symmetric memory)."""
+
+    def send_slot_header(self, rid, sid, rows, width, slot, row0, last):
+        h = torch.tensor([rid, sid, rows, width, slot, row0, int(last), 0], dtype=torch.int64)
+        self.dist.send(h, 0, group=self._g(self.ctrl, self.rank))
+
+    def _peer_arrival(self, src, rid, sid, rows, width, slot, row0, last):
+        self.ready.put((rid, sid, torch.tensor([src, rows, width, slot, row0, int(last)])))
+
+
+def _slot_worker(rank, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    ch = _SlotRecordingChannel(rank, 2, torch.device("cpu"), torch.float32)
+    if rank == 1:
+        ch.send_slot_header(7, 0, 1601, 7680, 1, 0, False)
+        ch.send(8, 0, torch.full((3, 4), 2.0))            # payload path in between
+        ch.send_slot_header(7, 1, 3202, 7680, 1, 1601, True)
+        ch.close()
+    else:
+        got = {}
+        while ch.finished_sources() < 1:
+            for rid, sid, t in ch.poll():
+                got[(rid, sid)] = t.tolist()
+        q.put((sorted(got.items()), dict(ch.counts)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_shard_channel_slot_headers_gloo_world2():
+    """The 8-int header: slot >= 0 means the rows are already in the receiver's memory."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_slot_worker, args=(r, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got, counts = q.get(timeout=120)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert counts == {"peer": 2, "nccl": 1}
+    assert got == [((7, 0), [1, 1601, 7680, 1, 0, 0]), ((7, 1), [1, 3202, 7680, 1, 1601, 1]),
+                   ((8, 0), [[2.0] * 4] * 3)]
