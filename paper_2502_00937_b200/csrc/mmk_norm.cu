@@ -9,10 +9,6 @@
 
 namespace mmk {
 
-#ifndef MMK_LN_MINB
-#define MMK_LN_MINB 1
-#endif
-
 MMK_DEV float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -63,7 +59,7 @@ MMK_DEV void store_row(void* y, int y_f32, int64_t row, int d, const float4 (&x)
 }
 
 template <int VEC>
-__global__ void __launch_bounds__(256, MMK_LN_MINB)
+__global__ void __launch_bounds__(256)
 layernorm_kernel(const float* __restrict__ x, void* y, int y_f32, int rows, int d, const float* __restrict__ gamma,
                  const float* __restrict__ beta, float eps, const float* __restrict__ tile_add,
                  const int32_t* __restrict__ tile_image, const int32_t* __restrict__ image_table,
