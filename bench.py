@@ -253,14 +253,35 @@ def main():
     staged = stage_images(imgs)  # resident uint8 images in HBM (the `value` leg)
     tiles = [core.tile_count(w, h, spec) for w, h in dims]
     flops_per_step = encoder_flops(spec, tiles)
-    handoff = Handoff(rank, world) if world > 1 else None
     # the receiver computes every source's row count itself from the deterministic plan
     rank_rows = {r: sum(core.tile_count(w, h, spec) for w, h in all_dims[r * B:(r + 1) * B]) * spec.tokens_per_tile
                  for r in range(world)}
+    # handoff of every rank's packed rows to the LLM-backend rank 0: K9+K10 fused (each rank's
+    # pack writes its rows straight into its region of rank 0's symmetric-memory prefill buffer
+    # over NVLink); NCCL point-to-point (dp.Handoff) if symmetric memory is unavailable
+    handoff, out_alloc, handoff_kind = None, None, None
+    if world > 1:
+        try:
+            import torch.distributed._symmetric_memory as symm
+            enc = spec.encoder
+            width = enc.hidden * (1 + len(enc.out_layers)) if enc.family == "mllama" else enc.hidden
+            first = [sum(rank_rows[q] for q in range(r)) * width for r in range(world)]
+            prefill = symm.empty(sum(rank_rows.values()) * width, dtype=torch.bfloat16, device="cuda")
+            hdl = symm.rendezvous(prefill, dist.group.WORLD)
+            my_slot = hdl.get_buffer(0, (rank_rows[rank], width), torch.bfloat16, first[rank])
+
+            def out_alloc(rows, w, _slot=my_slot):
+                assert (rows, w) == tuple(_slot.shape), (rows, w, tuple(_slot.shape))
+                return _slot
+            handoff_kind = "nvlink-pack-into-rank0"
+        except Exception as exc:  # noqa: BLE001 — no peer memory: NCCL send/recv instead
+            if rank == 0:
+                print(f"symmetric memory unavailable ({str(exc)[:120]}); NCCL handoff", file=sys.stderr)
+            handoff, handoff_kind = Handoff(rank, world), "p2p-handoff-to-rank0"
     stream = torch.cuda.current_stream()
 
     def step(batch):
-        out = ex.encode(batch)
+        out = ex.encode(batch, out_alloc=out_alloc)
         if handoff is not None:
             handoff.send(out, sizes=rank_rows)
         return out
@@ -271,7 +292,7 @@ def main():
         torch.cuda.synchronize()
 
     # the step as one CUDA graph (K0 -> K9, ~290 launches for Mllama): replayed in the timed region
-    captured = ex.capture(staged)
+    captured = ex.capture(staged, out_alloc=out_alloc)
 
     def step_graph():
         out = captured.replay()
@@ -318,7 +339,7 @@ def main():
         b = b_next
         if s_i + 1 < args.steps:  # the next step's H2D overlaps this step's encode
             b_next = stage_images(pinned_imgs, stream=copy_stream)
-        o = ex.encode(b)
+        o = ex.encode(b, out_alloc=out_alloc)
         if handoff is not None:
             handoff.send(o, sizes=rank_rows)
         ops.checksum(o.embeds, out=ck)
@@ -419,7 +440,7 @@ def main():
                        "tiles_per_gpu_per_step": int(sum(tiles)),
                        "tokens_per_gpu_per_step": int(sum(tiles)) * spec.tokens_per_tile,
                        "l2": "inputs > L2 (activations of one step are several GB)",
-                       "parallelism": f"dp{world}" + ("+p2p-handoff-to-rank0" if world > 1 else "")},
+                       "parallelism": f"dp{world}" + (f"+{handoff_kind}" if world > 1 else "")},
             "roofline": roof_entry(dominant), "roofline_other": roof_entry("gemm" if dominant == "attention" else "attention"),
             "roofline_step": {"achieved": round(enc_tf, 1), "peak": sus, "unit": "TFLOP/s",
                               "frac": round(enc_tf / sus, 4),

@@ -223,14 +223,15 @@ class ImagePathExecutor:
         return PackedBatch(embeds=emb, tok_offsets=plan["tok_off"], tiles=tiles,
                            image_tokens=[t * spec.tokens_per_tile for t in tiles])
 
-    def capture(self, batch: ImageBatch) -> "CapturedEncode":
+    def capture(self, batch: ImageBatch, out_alloc=None) -> "CapturedEncode":
         """Record ``encode(batch)`` as a CUDA graph (static shapes: same images each replay, or
-        new pixels copied into ``batch.src``).  Replay launches the whole path with one call."""
-        self.encode(batch)  # first run outside capture: kernel attributes, allocator warm-up
+        new pixels copied into ``batch.src``).  Replay launches the whole path with one call.
+        ``out_alloc`` must return the same buffer on every call (e.g. a fixed peer slot)."""
+        self.encode(batch, out_alloc=out_alloc)  # first run outside capture: kernel attributes, allocator warm-up
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            out = self.encode(batch)
+            out = self.encode(batch, out_alloc=out_alloc)
         return CapturedEncode(graph=g, batch=batch, output=out)
 
     def encode_images(self, images, pinned: bool = True, out_alloc=None) -> PackedBatch:
