@@ -113,6 +113,16 @@ def test_preprocess_mllama_bit_exact(mk):
     _check_preprocess(core, ops, encoders, spec, dims)
 
 
+@pytest.mark.parametrize("model", ["llama3.2-11b", "llava-clip-l14-336", "vit-b16-224"])
+def test_preprocess_generator_extremes_bit_exact(mk, model):
+    """The generator's clip range (64..4096 px per side, workload.py:143-178): largest images,
+    extreme aspect ratios in both orientations, and one-pixel strips."""
+    core, ops, encoders = mk
+    spec = core.get_model_spec(model)
+    dims = [(4096, 4096), (64, 4096), (4096, 64), (300, 4096), (4095, 1), (1, 4095), (64, 65)]
+    _check_preprocess(core, ops, encoders, spec, dims, seed=17)
+
+
 def test_preprocess_clip_bit_exact(mk):
     core, ops, encoders = mk
     for name in ("vit-b16-224", "llava-clip-l14-336"):
