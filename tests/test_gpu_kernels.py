@@ -385,3 +385,30 @@ def test_plain_c_client_of_the_abi(mk):
     assert r.returncode == 0, r.stderr
     assert "tok_off 0 3202 8005" in r.stdout  # reference tile_count: 1000x500 -> 2, 560x1200 -> 3
     assert "bad-arg status ok" in r.stdout
+
+
+def test_abi_status_codes_map_to_reference_exceptions(mk):
+    """MMK_ERR_ARG -> SpecError, MMK_ERR_UNSUPPORTED -> ProfileError (reference core.py:26-27,
+    profiles.py:23-24); the message names the kernel and the offending argument."""
+    _, ops, _ = mk
+    from paper_2502_00937_b200._lib import ProfileError
+    from paper_2502_00937_b200.core import SpecError
+    a = torch.randn(64, 64, device="cuda").bfloat16()
+    with pytest.raises(ProfileError, match="multiple of 32"):
+        ops.gemm(a, torch.randn(33, 64, device="cuda").bfloat16())          # N % 32 != 0
+    with pytest.raises(SpecError, match="16-byte"):
+        ops.gemm(a, torch.randn(64, 64, device="cuda").bfloat16(), bias=torch.randn(65, device="cuda")[1:])
+    qkv = torch.randn(10, 3 * 72, device="cuda").bfloat16()
+    cu = torch.tensor([0, 10], dtype=torch.int32, device="cuda")
+    with pytest.raises(ProfileError, match="head_dim"):
+        ops.attention(qkv, cu, 1, 10, 1, 72)
+    fin = torch.randn(8, 64, device="cuda")
+    inter = torch.randn(9, 8, 64, device="cuda").bfloat16()
+    with pytest.raises(ProfileError, match="n_inter"):
+        ops.pack_mllama(fin, inter)
+    out = torch.empty(8 * 64 * 2 + 8, dtype=torch.bfloat16, device="cuda")[1:1 + 8 * 128].view(8, 128)
+    with pytest.raises(SpecError, match="aligned"):
+        ops.pack_mllama(fin, inter[:1], out=out, peer=True)                  # 2-byte offset
+    # the context stays usable after every rejected call
+    torch.cuda.synchronize()
+    assert torch.equal(ops.pack_mllama(fin, inter[:1], peer=True), ops.pack_mllama(fin, inter[:1]))
