@@ -206,7 +206,9 @@ def _attn_ref(qkv, lens, heads, hd):
                                            (80, 16, [1601 * t for t in (1, 4, 2, 3, 1, 1, 4, 2) * 4]),
                                            # n_seq == 256 (largest sorted schedule), lengths 0..700 with ties
                                            (64, 4, [(i * 37) % 701 for i in range(256)]),
-                                           (64, 12, [197] * 300)])                # n_seq > 256: natural order
+                                           (64, 12, [197] * 300),                 # n_seq > 256: natural order
+                                           (64, 2, [5] * 1000 + [577, 0, 1]),     # 1003 tiny sequences
+                                           (80, 1, [1601, 3202, 6404])])          # one head
 def test_attention_varlen(mk, hd, heads, lens):
     _, ops, _ = mk
     T = sum(lens)
