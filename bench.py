@@ -332,20 +332,33 @@ def main():
     h2d = d2h = 0
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    fixed_shape = bool(wl.get("fixed"))
+    if fixed_shape:
+        # fixed-size workload (the reference default, 224x224 single tiles): a server replays the
+        # captured step (CapturedEncode) after copying each step's pixels into its input buffer —
+        # one H2D of the page-locked batch per step, inside the timed region
+        host_batch = torch.cat([t.reshape(-1) for t in pinned_imgs]).pin_memory()
+        cap_e2e = ex.capture(stage_images(pinned_imgs), out_alloc=out_alloc)
+        barrier()
     e_start.record(stream)
     copy_stream = torch.cuda.Stream()
-    b_next = stage_images(pinned_imgs, stream=copy_stream)
+    b_next = None if fixed_shape else stage_images(pinned_imgs, stream=copy_stream)
     for s_i in range(args.steps):
-        b = b_next
-        if s_i + 1 < args.steps:  # the next step's H2D overlaps this step's encode
-            b_next = stage_images(pinned_imgs, stream=copy_stream)
-        o = ex.encode(b, out_alloc=out_alloc)
+        if fixed_shape:
+            cap_e2e.batch.src.copy_(host_batch, non_blocking=True)
+            o = cap_e2e.replay()
+            h2d += host_batch.numel()
+        else:
+            b = b_next
+            if s_i + 1 < args.steps:  # the next step's H2D overlaps this step's encode
+                b_next = stage_images(pinned_imgs, stream=copy_stream)
+            o = ex.encode(b, out_alloc=out_alloc)
+            h2d += b.h2d_bytes
         if handoff is not None:
             handoff.send(o, sizes=rank_rows)
         ops.checksum(o.embeds, out=ck)
         offs = o.tok_offsets.to("cpu", non_blocking=True)
         cks = ck.to("cpu", non_blocking=True)
-        h2d += b.h2d_bytes
         d2h += offs.numel() * 8 + 4
     if handoff is not None:
         handoff.flush()
@@ -454,7 +467,10 @@ def main():
             "gpu_launches": launches,
             "e2e": {"value": round(e_value, 3), "unit": "images/s", "h2d_bytes_per_step": h2d // args.steps,
                     "d2h_bytes_per_step": d2h // args.steps,
-                    "path": "ImagePathExecutor.encode(stage_images(pinned host uint8 images, per-image H2D on a side stream, next step staged during the current encode)) + checksum D2H"},
+                    "path": ("ImagePathExecutor.capture(...).replay() after one H2D of the page-locked batch into its "
+                             "input buffer (fixed-size workload) + checksum D2H" if fixed_shape else
+                             "ImagePathExecutor.encode(stage_images(pinned host uint8 images, per-image H2D on a side "
+                             "stream, next step staged during the current encode)) + checksum D2H")},
             "e2e_jpeg": e2e_jpeg,
             "clocks": clk.result(),
         }
