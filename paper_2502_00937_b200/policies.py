@@ -71,7 +71,7 @@ def route_image(request, instances, router: RouterKind, max_fanout: int, rr_stat
         return None
     tiles = [img.tiles for img in request.images]
     fanout = min(len(tiles), len(instances), max_fanout)
-    if router is RouterKind.ROUND_ROBIN:
+    if router == RouterKind.ROUND_ROBIN:  # by value: the reference's own enum members work too
         pool = sorted(instances, key=lambda inst: inst.id)
         start = rr_state.get("image", 0)
         rr_state["image"] = start + fanout
@@ -89,7 +89,7 @@ def schedule_order(items, now: float, scheduler: SchedulerKind, aging_slo_fracti
     """
     runnable = [i for i, it in enumerate(items) if it.runnable]
     fifo_key = lambda i: (items[i].enqueue_ms, items[i].seq)  # noqa: E731
-    if scheduler is SchedulerKind.FIFO:
+    if scheduler == SchedulerKind.FIFO:
         return sorted(runnable, key=fifo_key)
     aged = [i for i in runnable if now - items[i].enqueue_ms > aging_slo_fraction * items[i].ttft_slo_ms]
     aged_set = set(aged)

@@ -171,16 +171,39 @@ def parse_dims(cell: str) -> list[tuple[int, int]]:
     return dims
 
 
-def load_trace(path: str | Path, model: ModelSpec, max_malformed_frac: float = 0.01):
-    """Trace CSV -> (requests sorted by arrival, malformed rows, total rows)."""
+@dataclass
+class TraceRecord:
+    """One parsed trace row (reference workload.py:28-33)."""
+    arrival_ms: float
+    service_id: str
+    text_tokens: int
+    image_dims: list[tuple[int, int]]
+    output_tokens: int
+
+
+@dataclass
+class TraceLoadResult:
+    """``load_trace`` result (reference workload.py:36-40)."""
+    requests: list[Request]
+    malformed_rows: int
+    total_rows: int
+
+
+def load_trace(path: str | Path, model: ModelSpec, max_malformed_frac: float = 0.01) -> TraceLoadResult:
+    """Trace CSV -> requests sorted by arrival (reference workload.py:54-108).
+
+    Malformed rows are counted and skipped; a malformed share above ``max_malformed_frac``
+    raises ``TraceError``. Requests get ids 0..n-1 in arrival order.
+    """
     path = Path(path)
     if not path.exists():
         raise TraceError(f"trace file not found: {path}")
-    rows, bad, total = [], 0, 0
+    records: list[TraceRecord] = []
+    bad = total = 0
     with path.open(newline="") as fh:
         reader = csv.DictReader(fh)
         if reader.fieldnames is None:
-            return [], 0, 0
+            return TraceLoadResult([], 0, 0)
         missing = [c for c in TRACE_COLUMNS if c not in reader.fieldnames]
         if missing:
             raise TraceError(f"trace {path} missing columns: {missing}")
@@ -190,23 +213,27 @@ def load_trace(path: str | Path, model: ModelSpec, max_malformed_frac: float = 0
                 dims = parse_dims(row["image_dims"] or "")
                 if int(row["num_images"]) != len(dims):
                     raise ValueError("num_images does not match image_dims")
-                rec = (float(row["arrival_ms"]), row["service_id"] or "default", int(row["text_tokens"]),
-                       dims, int(row["output_tokens"]))
-                if rec[0] < 0 or rec[2] < 0 or rec[4] < 1:
+                rec = TraceRecord(arrival_ms=float(row["arrival_ms"]),
+                                  service_id=row["service_id"] or "default",
+                                  text_tokens=int(row["text_tokens"]), image_dims=dims,
+                                  output_tokens=int(row["output_tokens"]))
+                if rec.arrival_ms < 0 or rec.text_tokens < 0 or rec.output_tokens < 1:
                     raise ValueError("negative counts")
-                rows.append(rec)
+                records.append(rec)
             except (ValueError, KeyError):
                 bad += 1
     if total and bad / total > max_malformed_frac:
         raise TraceError(f"{bad}/{total} malformed rows in {path} exceeds {max_malformed_frac:.0%}")
-    rows.sort(key=lambda r: r[0])
-    reqs = [Request(id=i, arrival_ms=a, text_tokens=tt, output_tokens=o, service_id=s,
-                    images=tuple(ImageSpec.from_dims(w, h, model) for w, h in dims))
-            for i, (a, s, tt, dims, o) in enumerate(rows)]
-    return reqs, bad, total
+    records.sort(key=lambda r: r.arrival_ms)
+    reqs = [Request(id=i, arrival_ms=r.arrival_ms, text_tokens=r.text_tokens,
+                    output_tokens=r.output_tokens, service_id=r.service_id,
+                    images=tuple(ImageSpec.from_dims(w, h, model) for w, h in r.image_dims))
+            for i, r in enumerate(records)]
+    return TraceLoadResult(reqs, bad, total)
 
 
 def write_trace(path: str | Path, requests: list[Request]) -> None:
+    """Requests -> trace CSV, the inverse of ``load_trace`` (reference workload.py:111-121)."""
     with Path(path).open("w", newline="") as fh:
         wr = csv.writer(fh)
         wr.writerow(TRACE_COLUMNS)

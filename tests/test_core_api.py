@@ -65,7 +65,9 @@ def test_presets_and_user_spec(tmp_path):
         assert name in specs
     assert specs["llama3.2-11b"].encoder.family == "mllama"
     assert specs["llama3.2-11b"].encoder.head_dim == 80
-    assert specs["llava-clip-l14-336"].encoder.head_dim == 64
+    assert len(specs) == 6  # exactly the reference's presets (reference test_core.py:100-102)
+    assert core.get_model_spec("llava-clip-l14-336").encoder.head_dim == 64
+    assert set(core.encoder_presets()) == {"vit-b16-224", "llava-clip-l14-336"}
     with pytest.raises(SpecError):
         core.get_model_spec("gpt-oss-999t")
     path = tmp_path / "m.json"
