@@ -37,8 +37,9 @@ def _act(x, act):
     return x * torch.sigmoid(1.702 * x)
 
 
-def _layer(h, W, pre, heads, act, eps, gated=False):
-    """One pre-LN transformer block on a single image's tokens h [S, d]."""
+def _layer(h, W, pre, heads, act, eps, gated=False, mask=None):
+    """One pre-LN transformer block on a single image's tokens h [S, d] (``mask``: optional
+    additive [S, S] attention bias, used only by the HF-faithful Mllama mode)."""
     S, d = h.shape
     hd = d // heads
     x = _ln(h, W[pre + "ln1_w"], W[pre + "ln1_b"], eps)
@@ -49,7 +50,7 @@ def _layer(h, W, pre, heads, act, eps, gated=False):
     q = q.view(S, heads, hd).transpose(0, 1)
     k = k.view(S, heads, hd).transpose(0, 1)
     v = v.view(S, heads, hd).transpose(0, 1)
-    a = Fn.scaled_dot_product_attention(q[None], k[None], v[None], scale=hd ** -0.5)[0]
+    a = Fn.scaled_dot_product_attention(q[None], k[None], v[None], attn_mask=mask, scale=hd ** -0.5)[0]
     a = a.transpose(0, 1).reshape(S, d) @ W[pre + "o_w"].t()
     if W.get(pre + "o_b") is not None:
         a = a + W[pre + "o_b"]
@@ -78,8 +79,8 @@ def clip_image(patches: torch.Tensor, W, enc) -> torch.Tensor:
     n_run = enc.layers if enc.out_layer == -1 else enc.layers + 1 + enc.out_layer
     for i in range(n_run):
         h = _layer(h, W, f"l{i}.", enc.heads, enc.act, eps)
-    if enc.out_layer == -1:
-        h = _ln(h, W["post_ln_w"], W["post_ln_b"], eps)
+    # hidden_states[out_layer] of CLIPVisionModel: post_layernorm is applied to the pooled CLS
+    # only (modeling_clip.py), never to the emitted sequence
     return h[1:] if enc.drop_cls else h
 
 
@@ -104,8 +105,53 @@ def mllama_image(patches: torch.Tensor, W, enc, ar_id: int, n_tiles: int) -> tor
     h = h.reshape(n_tiles * (P + 1), d)
     for i in range(enc.global_layers):
         h = _layer(h, W, f"g{i}.", enc.heads, enc.act, eps, gated=True)
-    inter = torch.stack([hidden[i] for i in enc.out_layers], dim=-1).reshape(h.shape[0], -1)
+    # hidden[j] = input of local layer j = output of layer j-1 (Meta / transformers 4.x);
+    # out_layers_of="output" (transformers 5.x) names the output of layer i = hidden[i + 1]
+    shift = 0 if getattr(enc, "out_layers_of", "input") == "input" else 1
+    inter = torch.stack([hidden[i + shift] for i in enc.out_layers], dim=-1).reshape(h.shape[0], -1)
     return torch.cat([h, inter], dim=-1)
+
+
+def mllama_image_hf(patches: torch.Tensor, W, enc, ar_id: int, n_tiles: int, max_tiles: int) -> torch.Tensor:
+    """HF-faithful Mllama forward (TEST INFRASTRUCTURE, pins the structure of ``mllama_image``
+    against transformers' MllamaVisionModel, modeling_mllama.py:930-1037): every image carries
+    ``max_tiles`` tile slots (patches [max_tiles*P, k], padded slots as given), every tile's
+    P+1 tokens are zero-padded to a multiple of 8 after layernorm_pre, and attention uses HF's
+    mask (_prepare_aspect_ratio_attention_mask, :77-102), which masks only pairs where BOTH the
+    query and the key are padding (pad patch or padded tile).  Returns the real tiles' tokens,
+    [n_tiles*(P+1), d*(1+len(out_layers))] — the product's ragged layout."""
+    eps, d, heads = enc.norm_eps, enc.hidden, enc.heads
+    P = patches.shape[0] // max_tiles
+    x = patch_embed(patches, W).view(max_tiles, P, d)
+    x = x + math.tanh(float(W["pre_gate"])) * W["pre_tile"][ar_id, :max_tiles, None, :]
+    x = torch.cat([W["cls"].expand(max_tiles, 1, d), x], 1)
+    g = math.tanh(float(W["pos_gate"]))
+    x = x + (1.0 - g) * W["pos"][None] + g * W["tile_pos"][ar_id, :max_tiles]
+    x = _ln(x, W["pre_ln_w"], W["pre_ln_b"], eps)
+    P1 = P + 1
+    P8 = -(-P1 // 8) * 8
+    x = Fn.pad(x, (0, 0, 0, P8 - P1))
+    pad_tok = torch.ones(max_tiles, P8, dtype=torch.bool)
+    pad_tok[:n_tiles, :P1] = False  # real tokens of real tiles
+    pad_tok = pad_tok.reshape(-1).float()
+    mask = (pad_tok[:, None] * pad_tok[None, :]) * torch.finfo(torch.float32).min
+    h = x.reshape(max_tiles * P8, d)
+    outs = []  # outputs of the local layers, as transformers 5.x collects them
+    for i in range(enc.layers):
+        h = _layer(h, W, f"l{i}.", heads, enc.act, eps, mask=mask)
+        outs.append(h)
+    h = _ln(h, W["post_ln_w"], W["post_ln_b"], eps).view(max_tiles, P8, d)
+    h = h + math.tanh(float(W["post_gate"])) * W["post_tile"][ar_id, :max_tiles, None, :]
+    h = h.reshape(max_tiles * P8, d)
+    for i in range(enc.global_layers):
+        h = _layer(h, W, f"g{i}.", heads, enc.act, eps, gated=True, mask=mask)
+    if getattr(enc, "out_layers_of", "input") == "input":
+        hidden = [None] + outs  # hidden[j] = input of layer j (j >= 1)
+    else:
+        hidden = outs
+    inter = torch.stack([hidden[i] for i in enc.out_layers], dim=-1).reshape(h.shape[0], -1)
+    full = torch.cat([h, inter], dim=-1).view(max_tiles, P8, -1)[:n_tiles, :P1]
+    return full.reshape(n_tiles * P1, -1)
 
 
 MLLAMA_ASPECT_RATIOS = [(1, 1), (1, 2), (1, 3), (1, 4), (2, 1), (2, 2), (3, 1), (4, 1)]

@@ -10,7 +10,8 @@ pkg/src/lmmsim/profiles.py:136-145, called from engine.py:693-703) with the real
 Families (EncoderSpec.family):
 * "clip"   pre-LN ViT (ViT-B/16-224, CLIP ViT-L/14-336 as used by LLaVA: layer -2, no CLS)
 * "mllama" Llama-3.2-Vision encoder: gated tile embeddings, 32 local + 8 gated global layers,
-           output = [final | interleaved hidden_states[3,7,15,23,30]] (7680 wide)
+           output = [final | interleaved hidden_states[3,7,15,23,30]] (7680 wide;
+           EncoderSpec.out_layers_of fixes which hidden state index i names)
 
 Residual stream in fp32 (HBM), GEMM operands in bf16, fp32 accumulation in TMEM.
 Weights are random-initialised from a seed (no checkpoints in this environment).
@@ -181,21 +182,20 @@ class DeviceEncoder:
             n_run = enc.layers if enc.out_layer == -1 else enc.layers + 1 + enc.out_layer
             for L in self.layers[:n_run]:
                 self._block(L, resid, x_buf, qkv_buf, h_buf, cu_seqlens, n_seq, max_seqlen)
+            # emitted = hidden_states[out_layer] as transformers' CLIPVisionModel numbers them
+            # (modeling_clip.py: post_layernorm touches only the pooled CLS, never the sequence)
             drop = 1 if enc.drop_cls else 0
             dst = out_alloc(total_tiles * (P + 1 - drop), d) if out_alloc is not None else None
-            if enc.out_layer == -1:
-                if drop == 0:
-                    return ops.layernorm(resid, *self.post_ln, enc.norm_eps, out=x_buf if dst is None else dst)
-                ops.layernorm(resid, *self.post_ln, enc.norm_eps, out=x_buf)
-                return ops.pack_drop_cls(x_buf, total_tiles, P + 1, drop, out=dst)
             return ops.pack_drop_cls(resid, total_tiles, P + 1, drop, out=dst)
         # ---------------- mllama
+        # intermediate capture: the FC2 epilogue of the layer whose output is the requested hidden
+        # state writes a bf16 copy (EncoderSpec.out_layers_of: Meta "input of layer i" or
+        # transformers-5 "output of layer i")
         outs = list(enc.out_layers)
-        if 0 in outs:
-            raise SpecError("mllama out_layers must be >= 1 (hidden_states[0] capture unsupported)")
         inter = torch.empty(len(outs), T, d, dtype=torch.bfloat16, device=dev)
         for i, L in enumerate(self.layers):
-            aux = inter[outs.index(i + 1)] if (i + 1) in outs else None
+            k = enc.capture_after(i)
+            aux = inter[k] if k is not None else None
             self._block(L, resid, x_buf, qkv_buf, h_buf, cu_seqlens, n_seq, max_seqlen, aux=aux)
         # layernorm_post + gated post-tile positional embedding, in place on the fp32 stream
         ops.layernorm(resid, *self.post_ln, enc.norm_eps, out=resid, out_f32=True, tile_add=self.post_tile_scaled,

@@ -20,9 +20,11 @@ from oracle import tiling as otiling  # noqa: E402
 REL_TOL = 1e-2
 
 
-def _reduced(spec, layers, global_layers=None, out_layers=None):
+def _reduced(spec, layers, global_layers=None, out_layers=None, out_layers_of=None):
     enc = spec.encoder
     kw = {"layers": layers}
+    if out_layers_of is not None:
+        kw["out_layers_of"] = out_layers_of
     if global_layers is not None:
         kw["global_layers"] = global_layers
     if out_layers is not None:
@@ -64,6 +66,15 @@ def test_mllama_reduced_depth():
     _run(spec, [(560, 560), (1000, 500), (1500, 1200), (300, 2000), (1120, 1120)])
 
 
+def test_mllama_reduced_depth_transformers5_capture():
+    """out_layers_of="output" (transformers 5.x numbering: hidden_states[i] = output of layer i,
+    index 0 allowed): the FC2-epilogue capture moves one layer earlier, oracle pinned to HF."""
+    from paper_2502_00937_b200 import core
+    spec = _reduced(core.get_model_spec("llama3.2-11b"), layers=4, global_layers=1, out_layers=[0, 1, 3],
+                    out_layers_of="output")
+    _run(spec, [(560, 560), (1300, 600)], seed=4)
+
+
 def test_mllama_full_depth_one_image():
     from paper_2502_00937_b200 import core
     spec = core.get_model_spec("llama3.2-11b")
@@ -77,6 +88,7 @@ def test_clip_l336_llava_penultimate():
 
 
 def test_vit_b16_batch8():
+    """out_layer=-1: last_hidden_state, no post-LN on the sequence (as CLIPVisionModel)."""
     from paper_2502_00937_b200 import core
     spec = core.get_model_spec("vit-b16-224")
     _run(spec, [(224, 224)] * 8, seed=2)

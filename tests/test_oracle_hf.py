@@ -86,6 +86,11 @@ def test_clip_vision_hidden_states_match_hf():
     enc = SimpleNamespace(norm_eps=1e-5, layers=layers, heads=heads, act="quick_gelu", drop_cls=True, out_layer=-2)
     ours = oenc.clip_image(patches, W, enc)
     torch.testing.assert_close(ours, hf[-2][0, 1:], rtol=1e-4, atol=1e-4)
+    # out_layer=-1 emits last_hidden_state: HF applies post_layernorm to the pooled CLS only
+    enc_last = SimpleNamespace(norm_eps=1e-5, layers=layers, heads=heads, act="quick_gelu", drop_cls=False,
+                               out_layer=-1)
+    out = m(pixel_values=px)
+    torch.testing.assert_close(oenc.clip_image(patches, W, enc_last), out.last_hidden_state[0], rtol=1e-4, atol=1e-4)
 
 
 @torch.no_grad()
@@ -161,3 +166,120 @@ def test_aspect_ratio_ids_follow_transformers():
     # and the closed form used by the K0 kernel
     for i, (a, b) in enumerate(ratios):
         assert b + sum(4 // k for k in range(1, a)) == i + 1
+
+
+def _mllama_reduced(out_layers, out_layers_of, layers=8, global_layers=2, T=56):
+    import dataclasses
+
+    from paper_2502_00937_b200 import core
+    base = core.get_model_spec("llama3.2-11b")
+    P1 = (T // 14) ** 2 + 1
+    enc = dataclasses.replace(base.encoder, layers=layers, global_layers=global_layers, ffn=1280,
+                              out_layers=tuple(out_layers), out_layers_of=out_layers_of)
+    return dataclasses.replace(base, tile_edge_px=T, tokens_per_tile=P1, encoder=enc)
+
+
+def _hf_mllama_from(W, spec, hf_indices):
+    from transformers.models.mllama.configuration_mllama import MllamaVisionConfig
+    from transformers.models.mllama.modeling_mllama import MllamaVisionModel
+    enc = spec.encoder
+    d, p, T = enc.hidden, enc.patch_px, spec.tile_edge_px
+    cfg = MllamaVisionConfig(hidden_size=d, intermediate_size=enc.ffn, attention_heads=enc.heads,
+                             num_hidden_layers=enc.layers, num_global_layers=enc.global_layers, image_size=T,
+                             patch_size=p, max_num_tiles=spec.max_tiles_per_image, hidden_act="gelu",
+                             norm_eps=enc.norm_eps, intermediate_layers_indices=list(hf_indices))
+    m = MllamaVisionModel(cfg).eval()
+    m.patch_embedding.weight.data.copy_(W["patch_w"].view(d, 3, p, p))
+    m.class_embedding.data.copy_(W["cls"])
+    gp = m.gated_positional_embedding
+    gp.gate.data.copy_(W["pos_gate"])
+    gp.embedding.data.copy_(W["pos"])
+    gp.tile_embedding.weight.data.copy_(W["tile_pos"].reshape(W["tile_pos"].shape[0], -1))
+    m.pre_tile_positional_embedding.gate.data.copy_(W["pre_gate"])
+    m.pre_tile_positional_embedding.embedding.weight.data.copy_(W["pre_tile"].reshape(W["pre_tile"].shape[0], -1))
+    m.post_tile_positional_embedding.gate.data.copy_(W["post_gate"])
+    m.post_tile_positional_embedding.embedding.weight.data.copy_(W["post_tile"].reshape(W["post_tile"].shape[0], -1))
+    for nm, mod in (("pre_ln", m.layernorm_pre), ("post_ln", m.layernorm_post)):
+        mod.weight.data.copy_(W[nm + "_w"])
+        mod.bias.data.copy_(W[nm + "_b"])
+    for stack, tag in ((m.transformer.layers, "l"), (m.global_transformer.layers, "g")):
+        for i, layer in enumerate(stack):
+            pre = f"{tag}{i}."
+            q, k, v = W[pre + "qkv_w"].split(d, 0)
+            layer.self_attn.q_proj.weight.data.copy_(q)
+            layer.self_attn.k_proj.weight.data.copy_(k)
+            layer.self_attn.v_proj.weight.data.copy_(v)
+            layer.self_attn.o_proj.weight.data.copy_(W[pre + "o_w"])
+            layer.input_layernorm.weight.data.copy_(W[pre + "ln1_w"])
+            layer.input_layernorm.bias.data.copy_(W[pre + "ln1_b"])
+            layer.post_attention_layernorm.weight.data.copy_(W[pre + "ln2_w"])
+            layer.post_attention_layernorm.bias.data.copy_(W[pre + "ln2_b"])
+            layer.mlp.fc1.weight.data.copy_(W[pre + "fc1_w"])
+            layer.mlp.fc1.bias.data.copy_(W[pre + "fc1_b"])
+            layer.mlp.fc2.weight.data.copy_(W[pre + "fc2_w"])
+            layer.mlp.fc2.bias.data.copy_(W[pre + "fc2_b"])
+            if tag == "g":
+                layer.gate_attn.data.copy_(W[pre + "gate_attn"])
+                layer.gate_ffn.data.copy_(W[pre + "gate_ffn"])
+    return m
+
+
+@torch.no_grad()
+def test_mllama_full_model_matches_hf():
+    """The whole MllamaVisionModel (transformers 5.5 here, random weights, every gate != 0) vs the
+    oracle's HF-faithful mode on 1-, 2-, 3- and 4-tile images (padded tile slots included): all
+    7680 output columns = final global-transformer output + 5 interleaved intermediate states.
+
+    Pins the out_layers convention both ways: transformers 5.x's ``hidden_states[i]`` is the
+    OUTPUT of local layer i (modeling_mllama.py:353-361, :1024), i.e. out_layers_of="output";
+    Meta's / transformers 4.x's index names the INPUT of layer i, i.e. the same tensors at
+    index + 1 (out_layers_of="input", the product default)."""
+    from paper_2502_00937_b200.encoders import init_weights
+    hf_idx = [1, 3, 5, 6, 7]
+    spec_out = _mllama_reduced(hf_idx, "output")
+    spec_in = _mllama_reduced([i + 1 for i in hf_idx], "input")
+    W = init_weights(spec_out, seed=3, gate_scale=0.8)
+    for g in ("pos_gate", "pre_gate", "post_gate"):
+        assert abs(float(W[g])) > 1e-3
+    m = _hf_mllama_from(W, spec_out, hf_idx)
+    T, p, max_t = spec_out.tile_edge_px, spec_out.encoder.patch_px, spec_out.max_tiles_per_image
+    P = (T // p) ** 2
+    g = torch.Generator().manual_seed(4)
+    for rows, cols in [(1, 1), (1, 2), (3, 1), (2, 2)]:
+        n = rows * cols
+        ar = oenc.aspect_ratio_id(rows, cols)
+        px = torch.randn(1, 1, max_t, 3, T, T, generator=g)
+        px[:, :, n:] = 0.0  # padded tile slots, as the HF processor leaves them
+        mask = torch.tensor([[[1] * n + [0] * (max_t - n)]])
+        hf = m(pixel_values=px, aspect_ratio_ids=torch.tensor([[ar]]), aspect_ratio_mask=mask).last_hidden_state
+        hf = hf[0, 0, :n].reshape(n * (P + 1), -1)
+        assert hf.shape[1] == 1280 * 6
+        patches = px[0, 0].unfold(2, p, p).unfold(3, p, p).permute(0, 2, 3, 1, 4, 5).reshape(max_t * P, 3 * p * p)
+        for spec in (spec_out, spec_in):
+            ours = oenc.mllama_image_hf(patches, W, spec.encoder, ar, n, max_t)
+            rel = ((ours - hf).norm() / hf.norm()).item()
+            assert rel < 1e-5, (rows, cols, spec.encoder.out_layers_of, rel)
+            torch.testing.assert_close(ours, hf, rtol=1e-3, atol=1e-3)
+
+
+@torch.no_grad()
+def test_mllama_ragged_oracle_equals_faithful_when_hf_pads_nothing():
+    """The product's ragged form (mllama_image: n_tiles*(P+1) tokens, no pad tokens) is the
+    faithful form minus HF's padding.  With P + 1 = 64 tokens per tile (already a multiple of 8)
+    and no padded tile slots the faithful form pads nothing, and both must agree: this carries
+    the HF pin above over to every term of the ragged oracle (embeddings, gates, LN_post +
+    post-tile, global layers, intermediate capture)."""
+    from paper_2502_00937_b200.encoders import init_weights
+    spec = _mllama_reduced([2, 4, 6, 7, 8], "input")
+    W = dict(init_weights(spec, seed=5, gate_scale=0.8))
+    P, d = 63, spec.encoder.hidden
+    g = torch.Generator().manual_seed(6)
+    W["pos"] = torch.randn(P + 1, d, generator=g) * d ** -0.5
+    W["tile_pos"] = torch.randn(9, 4, P + 1, d, generator=g) * 0.02
+    for rows, cols in [(1, 1), (1, 3), (2, 2)]:
+        n = rows * cols
+        ar = oenc.aspect_ratio_id(rows, cols)
+        patches = torch.randn(n * P, 3 * 14 * 14, generator=g)
+        ragged = oenc.mllama_image(patches, W, spec.encoder, ar, n)
+        faithful = oenc.mllama_image_hf(patches, W, spec.encoder, ar, n, n)
+        torch.testing.assert_close(ragged, faithful, rtol=1e-4, atol=1e-4)
