@@ -14,6 +14,7 @@
  * PINNED: tests/golden/tiling.json holds the reference's own tile_count / image_tokens for
  * ~4.7k dims x 9 specs; tests/test_oracle.py checks this file against it.
  */
+#include <math.h>
 #include <stdint.h>
 
 static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -63,18 +64,21 @@ void oracle_plan_one(int64_t w, int64_t h, int64_t T, int64_t cap, int thumb, in
   geom[1] = (int32_t)rows;
   geom[2] = (int32_t)cols;
   if (mode == 0) {
+    /* transformers get_image_size_fit_to_canvas (image_processing_mllama.py:82-130) in double,
+       as Python evaluates it: floor(dim * (target / dim_other)) */
     int64_t cw = cols * T, ch = rows * T;
     int64_t tw = w < T ? T : (w > cw ? cw : w);
     int64_t th = h < T ? T : (h > ch ? ch : h);
+    double scale_h = (double)th / (double)h, scale_w = (double)tw / (double)w;
     int64_t nw, nh;
-    if (tw * h < th * w) {
+    if (scale_w < scale_h) {
       nw = tw;
-      nh = (h * tw) / w;
+      nh = (int64_t)floor((double)h * scale_w);
       if (nh < 1) nh = 1;
       if (nh > th) nh = th;
     } else {
       nh = th;
-      nw = (w * th) / h;
+      nw = (int64_t)floor((double)w * scale_h);
       if (nw < 1) nw = 1;
       if (nw > tw) nw = tw;
     }

@@ -23,7 +23,8 @@ def build(force: bool = False) -> Path:
     src = HERE / "tile_plan.c"
     if force or not SO.exists() or SO.stat().st_mtime < src.stat().st_mtime:
         SO.parent.mkdir(parents=True, exist_ok=True)
-        subprocess.run(["gcc", "-O2", "-std=c99", "-shared", "-fPIC", str(src), "-o", str(SO)], check=True)
+        subprocess.run(["gcc", "-O2", "-std=c99", "-ffp-contract=off", "-shared", "-fPIC", str(src), "-o", str(SO), "-lm"],
+                       check=True)
     return SO
 
 

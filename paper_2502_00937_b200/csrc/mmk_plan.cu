@@ -8,8 +8,9 @@
 //   Request.total_tiles / total_image_tokens (core.py:110-120): exclusive int64 prefix sums
 // plus the builder-defined pixel geometry:
 //   rows x cols tile canvas (ceil grid when it fits the cap, else the best r*c == tiles
-//   arrangement by Mllama's scale criterion) and the resized image size (integer version of
-//   transformers' get_image_size_fit_to_canvas, or CLIP's shortest-edge resize).
+//   arrangement by Mllama's scale criterion) and the resized image size (transformers'
+//   get_image_size_fit_to_canvas in float64 as Python evaluates it, or CLIP's shortest-edge
+//   resize, int(T * long / short), which integer division reproduces exactly at these sizes).
 //
 // Two launches: a thread per image for the plan (tile count, canvas, aspect-ratio id), then one
 // CTA scanning the tile counts in coalesced 1024-image chunks (warp-shuffle + shared-memory scan,
@@ -68,17 +69,22 @@ __host__ __device__ inline TileGeom plan_one(int64_t w, int64_t h, int64_t T, in
   g.rows = static_cast<int32_t>(rows);
   g.cols = static_cast<int32_t>(cols);
   if (mode == 0) {
-    // integer get_image_size_fit_to_canvas: target = clip(dim, T, canvas)
+    // transformers' get_image_size_fit_to_canvas (image_processing_mllama.py:82-130), float64
+    // exactly as Python evaluates it: target = clip(dim, T, canvas); scale = target / dim;
+    // the other side = floor(dim * scale) (so 400x180 -> 560x251, not the rational 252).
+    // Division and multiply are single correctly rounded IEEE double ops on host and device.
     const int64_t cw = cols * T, ch = rows * T;
     const int64_t tw = w < T ? T : (w > cw ? cw : w);
     const int64_t th = h < T ? T : (h > ch ? ch : h);
+    const double scale_h = static_cast<double>(th) / static_cast<double>(h);
+    const double scale_w = static_cast<double>(tw) / static_cast<double>(w);
     int64_t nw, nh;
-    if (tw * h < th * w) {  // scale_w < scale_h
+    if (scale_w < scale_h) {
       nw = tw;
-      nh = (h * tw) / w; if (nh < 1) nh = 1; if (nh > th) nh = th;
+      nh = static_cast<int64_t>(floor(static_cast<double>(h) * scale_w)); if (nh < 1) nh = 1; if (nh > th) nh = th;
     } else {
       nh = th;
-      nw = (w * th) / h; if (nw < 1) nw = 1; if (nw > tw) nw = tw;
+      nw = static_cast<int64_t>(floor(static_cast<double>(w) * scale_h)); if (nw < 1) nw = 1; if (nw > tw) nw = tw;
     }
     g.new_w = static_cast<int32_t>(nw);
     g.new_h = static_cast<int32_t>(nh);

@@ -136,7 +136,9 @@ def test_preprocess_thumbnail_spec_bit_exact(mk):
     enc = core.EncoderSpec(family="clip", patch_px=14, hidden=128, ffn=256, layers=1, heads=2, resize_mode=0)
     spec = core.ModelSpec(name="thumb", architecture=core.Architecture.DEC_ONLY, tile_edge_px=448,
                           tokens_per_tile=1025, max_tiles_per_image=5, thumbnail_tile=True, encoder=enc)
-    dims = [(448, 448), (896, 448), (1500, 1500), (3000, 500), (200, 100)]
+    # (9000, 700): the thumbnail tile's source rows (27 KB) exceed the staging buffer, so the
+    # band reads them straight from global memory (the kernel's wide-row path)
+    dims = [(448, 448), (896, 448), (1500, 1500), (3000, 500), (200, 100), (9000, 700)]
     _check_preprocess(core, ops, encoders, spec, dims, seed=9)
 
 
@@ -292,23 +294,39 @@ def test_pack_drop_cls(mk):
     assert torch.equal(ops.pack_drop_cls(srcb, 4, 577, 0), srcb)
 
 
-def test_preprocess_chw_layout_bit_identical_to_hwc(mk):
+@pytest.mark.parametrize("thumb", [False, True])
+def test_preprocess_chw_layout_bit_identical_to_hwc(mk, thumb):
+    """CHW planes (the GPU JPEG decoder's layout) give the same patches as HWC, and both equal the
+    C oracle; the thumbnail case includes a 9000-px-wide image (wide-row path)."""
     core, ops, encoders = mk
     from paper_2502_00937_b200.executor import ImageBatch, stage_images
-    spec = core.get_model_spec("llama3.2-11b")
-    dims = [(700, 500), (1200, 1200), (64, 900)]
+    if thumb:
+        enc = core.EncoderSpec(family="clip", patch_px=14, hidden=128, ffn=256, layers=1, heads=2, resize_mode=0)
+        spec = core.ModelSpec(name="thumb", architecture=core.Architecture.DEC_ONLY, tile_edge_px=448,
+                              tokens_per_tile=1025, max_tiles_per_image=5, thumbnail_tile=True, encoder=enc)
+        dims = [(700, 500), (9000, 700), (64, 900)]
+    else:
+        spec = core.get_model_spec("llama3.2-11b")
+        dims = [(700, 500), (1200, 1200), (64, 900)]
     imgs = _rand_images(dims, 11)
     b = stage_images(imgs)
-    chw = torch.cat([torch.from_numpy(np.ascontiguousarray(i.transpose(2, 0, 1))).reshape(-1) for i in imgs]).cuda()
+    chw_imgs = [np.ascontiguousarray(i.transpose(2, 0, 1)) for i in imgs]
+    chw = torch.cat([torch.from_numpy(i).reshape(-1) for i in chw_imgs]).cuda()
     bc = ImageBatch(src=chw, src_off=b.src_off, w=b.w, h=b.h, dims=b.dims, chw=True)
     tiles = sum(core.tile_count(w, h, spec) for w, h in dims)
     plan = ops.tile_plan(b.w, b.h, spec)
     enc = spec.encoder
     scale, shift = oprep.norm_constants(enc.mean, enc.std)
-    args = (len(dims), tiles, spec, encoders.k_pad_of(spec), torch.from_numpy(scale).cuda(), torch.from_numpy(shift).cuda())
+    k_pad = encoders.k_pad_of(spec)
+    args = (len(dims), tiles, spec, k_pad, torch.from_numpy(scale).cuda(), torch.from_numpy(shift).cuda())
     a = ops.preprocess(b.src, b.src_off, b.w, b.h, plan["tile_off"], plan["geom"], *args)
     c = ops.preprocess(bc.src, bc.src_off, bc.w, bc.h, plan["tile_off"], plan["geom"], *args, chw=True)
     assert torch.equal(a, c)
+    oplan = otiling.tile_plan([d[0] for d in dims], [d[1] for d in dims], spec.tile_edge_px, spec.tokens_per_tile,
+                              spec.max_tiles_per_image, spec.thumbnail_tile, enc.resize_mode)
+    ref = oprep.preprocess(chw_imgs, oplan, spec.tile_edge_px, enc.patch_px, k_pad, enc.resize_mode,
+                           spec.thumbnail_tile, scale, shift, chw=True)
+    assert np.array_equal(c.view(torch.int16).cpu().numpy().view(np.uint16), ref)
 
 
 def test_gpu_jpeg_decode_path(mk):
