@@ -15,8 +15,17 @@ the token offsets + a checksum of the packed embeddings inside the timed region.
 rank encodes its own shard (weak scaling) and hands its packed embeddings to rank 0 (the
 LLM-backend GPU) with NCCL point-to-point sends inside the timed region (BASELINE configs[3]).
 
-``--impl reference`` times the CPU implementation of the path (the oracle port in oracle/:
-numpy preprocess + torch fp32 encoder, all host threads) on a bounded sample per step.
+Multi-GPU (``--gpus N`` under torchrun): the images are partitioned over the ranks by the path's
+own data-parallel partition (dp.partition_images with per-image encoder FLOPs, the cost-weighted
+form of the reference's split_by_tiles, policies.py:91-101) and every rank's packed rows are
+handed to rank 0 inside the timed region.  ``--scaling weak`` (default): N x B images per step,
+per-GPU work fixed; ``--scaling strong``: a fixed global batch (``--global-batch``) split N ways.
+
+``--impl reference`` times the CPU implementation of the path (the oracle port in oracle/: the C
+preprocess + torch fp32 encoder, all host threads) on the SAME workload: each step is one image
+(one image per tile count present in the batch, in turn), and images/s is the batch's time
+estimated from the per-tile-count means weighted by the batch's tile histogram.  It imports no
+product CUDA code (libmmk is never mapped).
 """
 
 from __future__ import annotations
@@ -40,6 +49,7 @@ WORKLOADS = {
     "llava-clip-l14-336": dict(config="LLaVA-style CLIP ViT-L/14-336, layer -2, CLS dropped, ragged packing",
                                batch=256, generator=dict()),
     "vit-b16-224": dict(config="reference default: 224x224 single tile -> ViT-B/16", batch=8, fixed=(224, 224)),
+
 }
 
 
@@ -51,8 +61,10 @@ def parse():
     ap.add_argument("--impl", default="mmk", choices=["mmk", "reference"])
     ap.add_argument("--model", default="llama3.2-11b", choices=sorted(WORKLOADS))
     ap.add_argument("--batch", type=int, default=0, help="images per GPU per step (0 = workload default)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--global-batch", type=int, default=0,
+                    help="strong scaling: images per step over all GPUs (0 = 4 x the workload batch)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-images", type=int, default=2)
     return ap.parse_args()
 
 
@@ -70,9 +82,16 @@ def image_dims(spec, n_images: int, seed: int = 0, fixed=None):
     return dims[:n_images]
 
 
-def make_images(dims, seed):
-    rng = np.random.default_rng(seed)
-    return [rng.integers(0, 256, (h, w, 3), dtype=np.uint8) for w, h in dims]
+def make_images(dims, seed, first_index: int = 0):
+    """Random uint8 pixels; image i of the workload is seeded by (seed, first_index + i), so an
+    image has the same pixels whichever rank encodes it."""
+    return [np.random.default_rng((seed, first_index + i)).integers(0, 256, (h, w, 3), dtype=np.uint8)
+            for i, (w, h) in enumerate(dims)]
+
+
+def images_at(dims, seed, indices):
+    return [np.random.default_rng((seed, i)).integers(0, 256, (dims[i][1], dims[i][0], 3), dtype=np.uint8)
+            for i in indices]
 
 
 def encoder_flops(spec, tiles_list):
@@ -160,16 +179,16 @@ def committed_traffic():
 
 
 # ----------------------------------------------------------------------------- CPU baseline
-def cpu_reference_time(spec, dims, weights, threads: int):
-    """Time the CPU path (oracle port: numpy preprocess + torch fp32 encoder) on the given images."""
+def cpu_reference_time(spec, imgs, weights, threads: int):
+    """Seconds of the CPU path (oracle port: C preprocess + torch fp32 encoder) on these images."""
     import torch
     from oracle import encoders as oenc
     from oracle import preprocess as oprep
     from oracle import tiling as otiling
-    from paper_2502_00937_b200.encoders import k_pad_of
+    from paper_2502_00937_b200.weights import k_pad_of
     torch.set_num_threads(threads)
     enc = spec.encoder
-    imgs = make_images(dims, 123)
+    dims = [(im.shape[1], im.shape[0]) for im in imgs]
     scale, shift = oprep.norm_constants(enc.mean, enc.std)
     t0 = time.perf_counter()
     plan = otiling.tile_plan([d[0] for d in dims], [d[1] for d in dims], spec.tile_edge_px, spec.tokens_per_tile,
@@ -181,33 +200,99 @@ def cpu_reference_time(spec, dims, weights, threads: int):
     return time.perf_counter() - t0
 
 
+class MixSampler:
+    """Same-config CPU sampling: one sample = one image of a tile count present in the batch (a
+    group of up to 8 images when the batch has a single tile count); the batch's CPU time is
+    estimated as sum over tile counts of (images with that count) x (mean seconds per image of
+    that count), tile counts never sampled scaled from the sampled ones by encoder FLOPs."""
+
+    def __init__(self, spec, dims, seed):
+        from paper_2502_00937_b200 import core
+        self.spec, self.dims, self.seed = spec, dims, seed
+        self.tiles = [core.tile_count(w, h, spec) for w, h in dims]
+        self.hist = {t: self.tiles.count(t) for t in sorted(set(self.tiles))}
+        self.group = min(8, len(dims)) if len(self.hist) == 1 else 1
+        self.order = sorted(self.hist, key=lambda t: -self.hist[t])  # most frequent tile count first
+        self.by_count = {t: [i for i, x in enumerate(self.tiles) if x == t] for t in self.hist}
+        self.times: dict = {t: [] for t in self.hist}
+        self.k = 0
+
+    def next_sample(self):
+        t = self.order[self.k % len(self.order)]
+        pool = self.by_count[t]
+        start = (self.k // len(self.order)) * self.group
+        idx = [pool[(start + j) % len(pool)] for j in range(self.group)]
+        self.k += 1
+        return t, images_at(self.dims, self.seed, idx)
+
+    def record(self, t, seconds):
+        self.times[t].append(seconds / self.group)
+
+    def batch_seconds(self):
+        per = {t: sum(v) / len(v) for t, v in self.times.items() if v}
+        flops = {t: encoder_flops(self.spec, [t]) for t in self.hist}
+        ref_t = max(per, key=lambda t: len(self.times[t]))
+        est = {t: per.get(t, per[ref_t] * flops[t] / flops[ref_t]) for t in self.hist}
+        return sum(self.hist[t] * est[t] for t in self.hist), est
+
+    def describe(self, est):
+        return {"tile_histogram": {str(t): c for t, c in self.hist.items()},
+                "seconds_per_image": {str(t): round(v, 3) for t, v in est.items()},
+                "samples": {str(t): len(v) * self.group for t, v in self.times.items()},
+                "same_config": True}
+
+
+def cpu_baseline_line(spec, dims, weights, seed, threads):
+    """One sample per tile count of the batch (~10-30 s of CPU work), weighted by the batch mix."""
+    ms = MixSampler(spec, dims, seed)
+    for _ in range(len(ms.hist)):
+        t, imgs = ms.next_sample()
+        ms.record(t, cpu_reference_time(spec, imgs, weights, threads))
+    total, est = ms.batch_seconds()
+    return {"value": round(len(dims) / total, 4), "unit": "images/s", "cores": threads, "kind": "port",
+            "sample": f"{ms.group} image(s) per tile count of the {len(dims)}-image batch, CPU time of the batch "
+                      f"estimated from the per-tile-count seconds weighted by its tile histogram (oracle C "
+                      f"preprocess + torch fp32 encoder, {threads} threads)",
+            **ms.describe(est)}
+
+
 def run_reference(args, spec, wl, rank, world, out=None):
-    """--impl reference: CPU implementation of the path on this box's host cores (rank 0 only)."""
+    """--impl reference: CPU implementation of the path on this box's host cores (rank 0 only),
+    on the GPU arm's workload (same image sizes and pixels), with no product CUDA code loaded."""
     if rank != 0:
         return
-    from paper_2502_00937_b200.encoders import init_weights
+    from paper_2502_00937_b200.weights import init_weights
     threads = len(os.sched_getaffinity(0))
     weights = init_weights(spec, 0)
-    dims = image_dims(spec, max(64, args.steps + args.warmup), fixed=wl.get("fixed"))
-    per_step = 1 if spec.encoder.family == "mllama" else max(1, min(8, wl["batch"]))
-    times, n_img = [], 0
-    for s in range(args.warmup + args.steps):
-        sample = [dims[(s * per_step + j) % len(dims)] for j in range(per_step)]
-        dt = cpu_reference_time(spec, sample, weights, threads)
-        if s >= args.warmup:
-            times.append(dt)
-            n_img += per_step
-    total = sum(times)
-    val = n_img / total
+    B = args.batch or wl["batch"]
+    G = B * world if args.scaling == "weak" else (args.global_batch or 4 * B)
+    dims = image_dims(spec, G, fixed=wl.get("fixed"))
+    ms = MixSampler(spec, dims, 1000)
+    step_s = []
+    for s_i in range(args.warmup + args.steps):
+        t, imgs = ms.next_sample()
+        dt = cpu_reference_time(spec, imgs, weights, threads)
+        if s_i >= args.warmup:
+            ms.record(t, dt)
+            step_s.append(dt)
+    total, est = ms.batch_seconds()
+    val = G / total
+    maps = open("/proc/self/maps").read() if os.path.exists("/proc/self/maps") else ""
+    native = sorted({ln.split()[-1] for ln in maps.splitlines() if ln.endswith(".so") and ROOT in ln})
+    assert not any("libmmk" in x for x in native), native  # the reference arm never maps product CUDA code
     line = {
         "impl": "reference", "metric": "images/sec (preprocess+encode)", "value": round(val, 4), "unit": "images/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1000 * total / len(times), 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": wl["config"], "model": spec.name, "images_per_step": per_step,
-                   "image_dims": "reference generator seed 0"},
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1000 * sum(step_s) / max(1, len(step_s)), 3),
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": wl["config"], "model": spec.name, "images_per_step_of_gpu_arm": G,
+                   "image_dims": "reference generator seed 0 (the GPU arm's batch)", "step": "one CPU sample"},
         "cpu_baseline": {"value": round(val, 4), "unit": "images/s", "cores": threads, "kind": "port",
-                         "sample": f"{per_step} image(s)/step from the reference generator dims, "
-                                   f"numpy preprocess + torch fp32 encoder on {threads} threads"},
+                         "sample": f"{ms.group} image(s) per step, cycling over the tile counts of the GPU arm's "
+                                   f"{G}-image batch; batch time = per-tile-count mean seconds x its tile histogram "
+                                   f"(oracle C preprocess + torch fp32 encoder on {threads} threads)",
+                         **ms.describe(est)},
+        "native_so_loaded": native,
         "e2e": {"value": round(val, 4), "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), file=out or sys.stdout, flush=True)
@@ -241,21 +326,26 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2502_00937_b200 import ops
-    from paper_2502_00937_b200.dp import Handoff
+    from paper_2502_00937_b200.dp import Handoff, partition_images
     from paper_2502_00937_b200.executor import ImagePathExecutor, stage_images
 
     B = args.batch or wl["batch"]
-    # every rank draws its own disjoint images (weak scaling: per-GPU work fixed as N grows)
-    all_dims = image_dims(spec, B * world, fixed=wl.get("fixed"))
-    dims = all_dims[rank * B:(rank + 1) * B]
-    imgs = make_images(dims, 1000 + rank)
+    # the step's images: weak scaling N x B (per-GPU work fixed), strong scaling a fixed global
+    # batch; partitioned over the ranks by the path's own DP partition weighted by encoder FLOPs
+    G = B * world if args.scaling == "weak" else (args.global_batch or 4 * B)
+    all_dims = image_dims(spec, G, fixed=wl.get("fixed"))
+    all_tiles = [core.tile_count(w, h, spec) for w, h in all_dims]
+    shards = partition_images(all_tiles, world, costs=[encoder_flops(spec, [t]) for t in all_tiles])
+    mine = shards[rank]
+    dims = [all_dims[i] for i in mine]
+    imgs = images_at(all_dims, 1000, mine)
     ex = ImagePathExecutor(spec, seed=0)
     staged = stage_images(imgs)  # resident uint8 images in HBM (the `value` leg)
-    tiles = [core.tile_count(w, h, spec) for w, h in dims]
+    tiles = [all_tiles[i] for i in mine]
     flops_per_step = encoder_flops(spec, tiles)
+    flops_job = encoder_flops(spec, all_tiles)
     # the receiver computes every source's row count itself from the deterministic plan
-    rank_rows = {r: sum(core.tile_count(w, h, spec) for w, h in all_dims[r * B:(r + 1) * B]) * spec.tokens_per_tile
-                 for r in range(world)}
+    rank_rows = {r: sum(all_tiles[i] for i in shards[r]) * spec.tokens_per_tile for r in range(world)}
     # handoff of every rank's packed rows to the LLM-backend rank 0: K9+K10 fused (each rank's
     # pack writes its rows straight into its region of rank 0's symmetric-memory prefill buffer
     # over NVLink); NCCL point-to-point (dp.Handoff) if symmetric memory is unavailable
@@ -295,6 +385,8 @@ def main():
     captured = ex.capture(staged, out_alloc=out_alloc)
 
     def step_graph():
+        if handoff is not None:  # the replay rewrites the buffer earlier sends may still be reading
+            handoff.release(captured.output.embeds)
         out = captured.replay()
         if handoff is not None:
             handoff.send(out, sizes=rank_rows)
@@ -318,7 +410,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = world * B * args.steps / (ms_max / 1000.0)
+    value = G * args.steps / (ms_max / 1000.0)
 
     # --------------------------------------------------------------- e2e through the public API
     # the step's inputs sit in pinned host memory (as a decoder writing page-locked buffers would
@@ -332,28 +424,15 @@ def main():
     h2d = d2h = 0
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
-    fixed_shape = bool(wl.get("fixed"))
-    if fixed_shape:
-        # fixed-size workload (the reference default, 224x224 single tiles): a server replays the
-        # captured step (CapturedEncode) after copying each step's pixels into its input buffer —
-        # one H2D of the page-locked batch per step, inside the timed region
-        host_batch = torch.cat([t.reshape(-1) for t in pinned_imgs]).pin_memory()
-        cap_e2e = ex.capture(stage_images(pinned_imgs), out_alloc=out_alloc)
-        barrier()
     e_start.record(stream)
     copy_stream = torch.cuda.Stream()
-    b_next = None if fixed_shape else stage_images(pinned_imgs, stream=copy_stream)
+    b_next = stage_images(pinned_imgs, stream=copy_stream)
     for s_i in range(args.steps):
-        if fixed_shape:
-            cap_e2e.batch.src.copy_(host_batch, non_blocking=True)
-            o = cap_e2e.replay()
-            h2d += host_batch.numel()
-        else:
-            b = b_next
-            if s_i + 1 < args.steps:  # the next step's H2D overlaps this step's encode
-                b_next = stage_images(pinned_imgs, stream=copy_stream)
-            o = ex.encode(b, out_alloc=out_alloc)
-            h2d += b.h2d_bytes
+        b = b_next
+        if s_i + 1 < args.steps:  # the next step's H2D overlaps this step's encode
+            b_next = stage_images(pinned_imgs, stream=copy_stream)
+        o = ex.encode(b, out_alloc=out_alloc)
+        h2d += b.h2d_bytes
         if handoff is not None:
             handoff.send(o, sizes=rank_rows)
         ops.checksum(o.embeds, out=ck)
@@ -368,8 +447,39 @@ def main():
     t = torch.tensor([e_ms], device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e_value = world * B * args.steps / (float(t.item()) / 1000.0)
+    e_value = G * args.steps / (float(t.item()) / 1000.0)
     assert np.isfinite(float(cks.item()))
+
+    # fixed-size workloads (the reference default, 224x224 single tiles): the path a server with a
+    # fixed batch shape would take — the step captured once, then per step one H2D of the
+    # page-locked batch into the captured input buffer and a replay (reported as e2e_graph)
+    e2e_graph = None
+    if wl.get("fixed"):
+        host_batch = torch.cat([t_.reshape(-1) for t_ in pinned_imgs]).pin_memory()
+        cap_e2e = ex.capture(stage_images(pinned_imgs), out_alloc=out_alloc)
+        barrier()
+        g_start, g_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g_start.record(stream)
+        for _ in range(args.steps):
+            if handoff is not None:
+                handoff.release(cap_e2e.output.embeds)
+            cap_e2e.batch.src.copy_(host_batch, non_blocking=True)
+            o = cap_e2e.replay()
+            if handoff is not None:
+                handoff.send(o, sizes=rank_rows)
+            ops.checksum(o.embeds, out=ck)
+            cks = ck.to("cpu", non_blocking=True)
+        if handoff is not None:
+            handoff.flush()
+        g_end.record(stream)
+        barrier()
+        t = torch.tensor([g_start.elapsed_time(g_end)], device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_graph = {"value": round(G * args.steps / (float(t.item()) / 1000.0), 3), "unit": "images/s",
+                     "h2d_bytes_per_step": int(host_batch.numel()), "d2h_bytes_per_step": 4,
+                     "path": "ImagePathExecutor.capture(...).replay() after one H2D of the page-locked batch into "
+                             "its input buffer + checksum D2H"}
 
     # --------------------------------------------------------------- e2e from JPEG bytes (GPU decode)
     e2e_jpeg = None
@@ -391,7 +501,7 @@ def main():
         t = torch.tensor([j_start.elapsed_time(j_end)], device="cuda")
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_jpeg = {"value": round(world * B * args.steps / (float(t.item()) / 1000.0), 3), "unit": "images/s",
+        e2e_jpeg = {"value": round(G * args.steps / (float(t.item()) / 1000.0), 3), "unit": "images/s",
                     "h2d_bytes_per_step": jb, "path": "ImagePathExecutor.encode_jpegs (nvJPEG decode on the GPU)"}
     except Exception as exc:  # torchvision without CUDA JPEG support: report why
         if os.environ.get("BENCH_DEBUG"):
@@ -442,16 +552,20 @@ def main():
                     "launches": k["launches"], "share_of_step": round(k["ms"] / ms_instr, 4) if ms_instr else None,
                     "timing": "per-launch CUDA events, eager repeat of the timed steps"}
 
-        enc_tf = flops_per_step / (step_ms / 1e3) / 1e12
+        enc_tf = flops_job / world / (step_ms / 1e3) / 1e12  # per GPU
         line = {
             "metric": "images/sec (preprocess+encode)", "value": round(value, 3), "unit": "images/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (reference generator image sizes, random uint8 pixels, random-init weights)",
             "config": {"workload": wl["config"] + (f", data-parallel over {world} B200" if world > 1 else ""),
-                       "model": spec.name, "images_per_gpu_per_step": B, "graph": "one CUDA graph per step",
-                       "tiles_per_gpu_per_step": int(sum(tiles)),
-                       "tokens_per_gpu_per_step": int(sum(tiles)) * spec.tokens_per_tile,
+                       "model": spec.name, "images_per_step": G, "images_rank0": len(dims),
+                       "graph": "one CUDA graph per step",
+                       "tiles_per_step": int(sum(all_tiles)), "tiles_rank0": int(sum(tiles)),
+                       "tile_histogram": {str(t): all_tiles.count(t) for t in sorted(set(all_tiles))},
+                       "tokens_per_step": int(sum(all_tiles)) * spec.tokens_per_tile,
+                       "partition": "dp.partition_images(costs=encoder FLOPs per image) (cost-weighted "
+                                    "split_by_tiles, reference policies.py:91-101)",
                        "l2": "inputs > L2 (activations of one step are several GB)",
                        "parallelism": f"dp{world}" + (f"+{handoff_kind}" if world > 1 else "")},
             "roofline": roof_entry(dominant), "roofline_other": roof_entry("gemm" if dominant == "attention" else "attention"),
@@ -467,22 +581,14 @@ def main():
             "gpu_launches": launches,
             "e2e": {"value": round(e_value, 3), "unit": "images/s", "h2d_bytes_per_step": h2d // args.steps,
                     "d2h_bytes_per_step": d2h // args.steps,
-                    "path": ("ImagePathExecutor.capture(...).replay() after one H2D of the page-locked batch into its "
-                             "input buffer (fixed-size workload) + checksum D2H" if fixed_shape else
-                             "ImagePathExecutor.encode(stage_images(pinned host uint8 images, per-image H2D on a side "
+                    "path": ("ImagePathExecutor.encode(stage_images(pinned host uint8 images, per-image H2D on a side "
                              "stream, next step staged during the current encode)) + checksum D2H")},
+            "e2e_graph": e2e_graph,
             "e2e_jpeg": e2e_jpeg,
             "clocks": clk.result(),
         }
         if not args.no_cpu_baseline and world == 1:
-            threads = len(os.sched_getaffinity(0))
-            sample = dims[:args.cpu_sample_images]
-            dt = cpu_reference_time(spec, sample, ex.weights, threads)
-            line["cpu_baseline"] = {"value": round(len(sample) / dt, 4), "unit": "images/s", "cores": threads,
-                                    "kind": "port",
-                                    "sample": f"first {len(sample)} images of the workload "
-                                              f"({sum(tiles[:len(sample)])} tiles), oracle numpy preprocess + "
-                                              f"torch fp32 encoder, {dt:.1f} s"}
+            line["cpu_baseline"] = cpu_baseline_line(spec, all_dims, ex.weights, 1000, len(os.sched_getaffinity(0)))
         print(json.dumps(line), file=result_out, flush=True)
     if world > 1:
         dist.barrier()

@@ -72,6 +72,12 @@ int mmk_tile_plan(const int32_t* w, const int32_t* h, int32_t n, int32_t tile_px
 int mmk_tile_index(const int64_t* tile_off, int32_t n, int32_t* tile_image, int32_t* tile_slot,
                    cudaStream_t stream);
 
+/* Attention sequence offsets of the varlen attention (one sequence per image):
+ * cu_seqlens[i] = tile_off[i] * seq_per_tile for i in [0, n] (int32; seq_per_tile = patches per
+ * tile + 1 class token).  Total sequence rows must stay below 2^31. */
+int mmk_seq_offsets(const int64_t* tile_off, int32_t n, int32_t seq_per_tile, int32_t* cu_seqlens,
+                    cudaStream_t stream);
+
 /*
  * K1 — fused uint8 HWC -> resize (bilinear, fp32) -> pad -> normalize -> tile -> patchify.
  *   src       : concatenated uint8 RGB images; src_off[n] byte offsets; src_chw = 0: HWC

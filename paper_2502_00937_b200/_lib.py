@@ -31,6 +31,7 @@ SIGNATURES = {
     "mmk_last_error": ([], ctypes.c_char_p),
     "mmk_tile_plan": ([_V, _V, _I32, _I32, _I32, _I32, _I32, _I32, _V, _V, _V, _V, _V, _V, _V], _I32),
     "mmk_tile_index": ([_V, _I32, _V, _V, _V], _I32),
+    "mmk_seq_offsets": ([_V, _I32, _I32, _V, _V], _I32),
     "mmk_preprocess": ([_V, _V, _I32, _V, _V, _V, _V, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _V, _V, _V, _V],
                        _I32),
     "mmk_gemm_bf16": ([_V, _I64, _V, _I64, _I32, _I32, _I32, _I32, _V, _V, _I64, _F, _V, _I64, _V], _I32),

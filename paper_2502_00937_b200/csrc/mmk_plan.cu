@@ -196,6 +196,16 @@ __global__ void tile_index_kernel(const int64_t* __restrict__ tile_off, int n, i
   }
 }
 
+// int32 attention offsets cu_seqlens[i] = tile_off[i] * seq_per_tile (i <= n): the sequences of
+// the varlen attention are whole images (all tiles of an image attend to each other).
+__global__ void seq_offsets_kernel(const int64_t* __restrict__ tile_off, int n, int seq_per_tile,
+                                   int32_t* __restrict__ cu_seqlens) {
+  griddep_wait();  // PDL: inputs come from the preceding kernel
+  griddep_launch_dependents();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i <= n) cu_seqlens[i] = static_cast<int32_t>(tile_off[i] * seq_per_tile);
+}
+
 }  // namespace mmk
 
 using namespace mmk;
@@ -224,4 +234,13 @@ extern "C" int mmk_tile_index(const int64_t* tile_off, int32_t n, int32_t* tile_
   (void)launch_kernel(tile_index_kernel, dim3((n + 7) / 8), dim3(block), 0, stream, 1, n <= 4096, tile_off, n, tile_image, tile_slot);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "tile_index: launch");
+}
+
+extern "C" int mmk_seq_offsets(const int64_t* tile_off, int32_t n, int32_t seq_per_tile, int32_t* cu_seqlens,
+                               cudaStream_t stream) {
+  if (n < 0 || seq_per_tile < 1) return set_error(MMK_ERR_ARG, "seq_offsets: n < 0 or seq_per_tile < 1");
+  (void)launch_kernel(seq_offsets_kernel, dim3(n / 256 + 1), dim3(256), 0, stream, 1, n <= 4096, tile_off, n,
+                      seq_per_tile, cu_seqlens);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "seq_offsets: launch");
 }

@@ -112,7 +112,6 @@ preprocess_kernel(const uint8_t* __restrict__ src, const int64_t* __restrict__ s
   __shared__ int s_srow[kMaxSlots];                   // source row of each slot (ascending)
   __shared__ int s_rowoff[kMaxSlots * 3];             // per (chunk slot, plane): stage byte of pixel 0
   __shared__ int s_xa, s_rs, s_cap, s_nslot;
-  __shared__ const uint8_t* s_buf_end;                // end of the source buffer (last image's last byte + 1)
   griddep_wait();  // PDL: inputs come from the preceding kernel
   griddep_launch_dependents();
 
@@ -148,8 +147,6 @@ preprocess_kernel(const uint8_t* __restrict__ src, const int64_t* __restrict__ s
       meta.nw = geom[4 * lo + 2];
       meta.nh = geom[4 * lo + 3];
       meta.off = src_off[lo];
-    } else if (tid == 1) {
-      s_buf_end = src + src_off[n - 1] + 3ll * w[n - 1] * h[n - 1];
     }
   } else if (tid < 38) {
     const int c = tid - 32;
@@ -330,10 +327,12 @@ preprocess_kernel(const uint8_t* __restrict__ src, const int64_t* __restrict__ s
     if (!direct) {
       if (sf > 0) __syncthreads();  // the previous chunk's rows are no longer read
       // stage: chunk slot s, plane c -> stage + (s*planes + c)*rs, copied from the 16-byte aligned
-      // address at or below the span start with asynchronous 16-byte copies (all in flight at
-      // once; the bytes around the span are the buffer's own, the buffer's last partial vector is
-      // zero-filled).  A warp per (slot, plane), lanes over the row's vectors.
-      const uint8_t* buf_end = s_buf_end;
+      // address at or below the span start with asynchronous 16-byte copies, all in flight at
+      // once.  Reads stay inside [align16_down(image), image end): the aligned bytes before an
+      // image share its allocation (allocations are >= 256-byte aligned), and the vector holding
+      // the image's last byte is zero-filled past it.  A warp per (slot, plane), lanes over the
+      // row's vectors.
+      const uint8_t* img_end = img + (CHW ? 3 * plane : row_bytes * m.h);
       const int nvec = rs >> 4;
       for (int r = wid; r < nsl * planes; r += nwarps) {
         const int s = CHW ? r / 3 : r, c = CHW ? r - 3 * s : 0;
@@ -343,20 +342,11 @@ preprocess_kernel(const uint8_t* __restrict__ src, const int64_t* __restrict__ s
         if (lane == 0) s_rowoff[r] = r * rs + static_cast<int>(span - gA) - bpp * xa;
         for (int v = lane; v < nvec; v += 32) {
           const uint8_t* gv = gA + 16 * v;
-          if (gv >= src) {
-            const int64_t left = buf_end - gv;
-            const uint32_t nb = left >= 16 ? 16u : (left > 0 ? static_cast<uint32_t>(left) : 0u);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + 16 * v), "l"(nb ? gv : src),
-                         "r"(nb)
-                         : "memory");
-          } else {  // an unaligned buffer start: bytes before it are not ours
-            uint32_t wv[4] = {0, 0, 0, 0};
-            for (int q = 0; q < 16; ++q)
-              if (gv + q >= src) wv[q >> 2] |= static_cast<uint32_t>(__ldg(gv + q)) << (8 * (q & 3));
-            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst + 16 * v), "r"(wv[0]), "r"(wv[1]),
-                         "r"(wv[2]), "r"(wv[3])
-                         : "memory");
-          }
+          const int64_t left = img_end - gv;
+          const uint32_t nb = left >= 16 ? 16u : (left > 0 ? static_cast<uint32_t>(left) : 0u);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + 16 * v), "l"(nb ? gv : img),
+                       "r"(nb)
+                       : "memory");
         }
       }
       asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");

@@ -9,7 +9,10 @@ rank (pull semantics of PAPER.md:654-660: the receiver posts the receives into a
 offsets it computes itself from the deterministic tile plan, so no size exchange is needed).
 
 Sends and receives are issued on NCCL's own stream and only waited on when their buffer is
-about to be reused (two steps later), so the transfer of step i overlaps compute of step i+1.
+about to be reused, so the transfer of step i overlaps compute of step i+1.  A sender whose
+packed output always lands in the same buffer (a replayed CUDA graph) calls ``release(buf)``
+before the kernels that rewrite it: the compute stream then waits for every pending send still
+reading that buffer (a stream wait, not a host sync).
 """
 
 from __future__ import annotations
@@ -43,6 +46,21 @@ class Handoff:
             works, _bufs = self.pending.popleft()
             for w in works:
                 w.wait()
+
+    def release(self, buf: torch.Tensor):
+        """Order the current stream after every pending send or receive that uses ``buf``'s
+        memory (call before rewriting a buffer that was handed to ``send``)."""
+        lo = buf.data_ptr()
+        hi = lo + buf.numel() * buf.element_size()
+        keep: deque = deque()
+        for works, payload in self.pending:
+            tensors = payload.values() if isinstance(payload, dict) else (payload,)
+            if any(t.data_ptr() < hi and lo < t.data_ptr() + t.numel() * t.element_size() for t in tensors):
+                for w in works:
+                    w.wait()
+            else:
+                keep.append((works, payload))
+        self.pending = keep
 
     def send(self, packed, sizes: dict | None = None, width: int | None = None):
         """packed: PackedBatch (or a tensor) of this rank.  On ``dst``, ``sizes`` maps source rank ->

@@ -37,6 +37,11 @@ class ImageBatch:
     h2d_bytes: int = 0
     chw: bool = False          # pixel layout of src: HWC (host decoders) or CHW planes (GPU JPEG decode)
     ready: "torch.cuda.Event | None" = None  # set when staged on a side stream: encode() waits on it
+    parts: tuple = ()          # separately allocated images src_off points into (GPU JPEG decode)
+
+    @property
+    def src_bytes(self) -> int:
+        return int(sum(w * h * 3 for w, h in self.dims))
 
     @property
     def n(self) -> int:
@@ -165,16 +170,22 @@ def stage_jpegs(jpegs, device="cuda") -> ImageBatch:
     for t in imgs:
         t.record_stream(compute)
     dims = [(int(t.shape[2]), int(t.shape[1])) for t in imgs]
-    sizes = np.array([w * h * 3 for w, h in dims], np.int64)
-    offs = np.zeros(len(imgs), np.int64)
-    offs[1:] = np.cumsum(sizes)[:-1]
-    src = torch.cat([t.reshape(-1) for t in imgs]) if imgs else torch.empty(0, dtype=torch.uint8, device=dev)
+    # no concatenation: K1 reads each decoded image where the decoder left it — src is the image
+    # at the lowest address and src_off[i] the byte distance of image i from it
+    n = len(imgs)
+    if n:
+        ptrs = np.array([t.data_ptr() for t in imgs], np.int64)
+        base = int(np.argmin(ptrs))
+        src = imgs[base]
+        offs = ptrs - ptrs[base]
+    else:
+        src, offs = torch.empty(0, dtype=torch.uint8, device=dev), np.zeros(0, np.int64)
     meta = np.concatenate([offs.view(np.int32), np.array([d[0] for d in dims], np.int32),
                            np.array([d[1] for d in dims], np.int32)])
     dmeta = torch.from_numpy(meta).pin_memory().to(dev, non_blocking=True)
-    n = len(imgs)
     return ImageBatch(src=src, src_off=dmeta[:2 * n].view(torch.int64), w=dmeta[2 * n:3 * n], h=dmeta[3 * n:4 * n],
-                      dims=dims, h2d_bytes=int(sum(d.numel() for d in datas)) + meta.nbytes, chw=True)
+                      dims=dims, h2d_bytes=int(sum(d.numel() for d in datas)) + meta.nbytes, chw=True,
+                      parts=tuple(imgs))
 
 
 class ImagePathExecutor:
@@ -200,7 +211,7 @@ class ImagePathExecutor:
         if batch.ready is not None:  # staged on a side stream: order after the copy, keep the memory
             compute = torch.cuda.current_stream(self.device)
             compute.wait_event(batch.ready)
-            for t in (batch.src, batch.src_off, batch.w, batch.h):
+            for t in (batch.src, batch.src_off, batch.w, batch.h, *batch.parts):
                 t.record_stream(compute)
         tiles = [tile_count(w, h, spec) for w, h in batch.dims]
         total_tiles = sum(tiles)
@@ -208,10 +219,10 @@ class ImagePathExecutor:
         plan = ops.tile_plan(batch.w, batch.h, spec)
         patches = ops.preprocess(batch.src, batch.src_off, batch.w, batch.h, plan["tile_off"], plan["geom"], n,
                                  total_tiles, spec, self.encoder.k_pad, self.encoder.norm_scale,
-                                 self.encoder.norm_shift, chw=batch.chw)
+                                 self.encoder.norm_shift, chw=batch.chw, src_bytes=batch.src_bytes)
         # attention sequences: all tokens of one image (images never attend to each other)
         seq_len = np.asarray(tiles, np.float64) * (P + 1)
-        cu = (plan["tile_off"] * (P + 1)).to(torch.int32)  # device-side: capturable in a CUDA graph
+        cu = ops.seq_offsets(plan["tile_off"], n, P + 1)  # device-side: capturable in a CUDA graph
         ops.set_attention_flops(cu, float(4 * np.sum(seq_len ** 2)))
         max_s = int(max(tiles)) * (P + 1)
         if enc.family == "mllama":

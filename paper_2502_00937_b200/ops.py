@@ -115,9 +115,21 @@ def tile_index(tile_off: torch.Tensor, n: int, total_tiles: int):
     return tile_image, tile_slot
 
 
+def seq_offsets(tile_off: torch.Tensor, n: int, seq_per_tile: int):
+    """int32 cu_seqlens [n+1] of the per-image attention sequences (one kernel, graph-capturable)."""
+    _need(tile_off, torch.int64, "tile_off")
+    cu = torch.empty(n + 1, dtype=torch.int32, device=tile_off.device)
+    _t0 = _begin()
+    _lib.check(_lib.lib.mmk_seq_offsets(tile_off.data_ptr(), n, seq_per_tile, cu.data_ptr(), _s()))
+    _end('tile_index', 0, _t0)
+    return cu
+
+
 def preprocess(src, src_off, w, h, tile_off, geom, n: int, total_tiles: int, spec, k_pad: int,
-               scale3: torch.Tensor, shift3: torch.Tensor, out: torch.Tensor | None = None, chw: bool = False):
-    """K1: uint8 images -> bf16 patch matrix [total_tiles * P, k_pad]."""
+               scale3: torch.Tensor, shift3: torch.Tensor, out: torch.Tensor | None = None, chw: bool = False,
+               src_bytes: int | None = None):
+    """K1: uint8 images -> bf16 patch matrix [total_tiles * P, k_pad].  ``src`` is the buffer
+    ``src_off`` counts from (ImageBatch.src); ``src_bytes`` the images' bytes (roofline log)."""
     enc = spec.encoder
     P = (spec.tile_edge_px // enc.patch_px) ** 2
     if out is None:
@@ -127,7 +139,7 @@ def preprocess(src, src_off, w, h, tile_off, geom, n: int, total_tiles: int, spe
                                        tile_off.data_ptr(), geom.data_ptr(), n, total_tiles, spec.tile_edge_px,
                                        enc.patch_px, k_pad, enc.resize_mode, int(spec.thumbnail_tile),
                                        scale3.data_ptr(), shift3.data_ptr(), out.data_ptr(), _s()))
-    _end('preprocess', float(src.numel()) + out.shape[0] * 3 * enc.patch_px ** 2 * 2.0, _t0)
+    _end('preprocess', float(src.numel() if src_bytes is None else src_bytes) + out.shape[0] * k_pad * 2.0, _t0)
     return out
 
 

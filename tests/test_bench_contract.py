@@ -21,6 +21,36 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"] == {"value": d["value"], "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     assert "workload" in d["config"]
+    # same config as the GPU arm (its batch's tile histogram) and no product CUDA code mapped
+    assert d["cpu_baseline"]["same_config"] is True and d["cpu_baseline"]["tile_histogram"] == {"1": 8}
+    assert not any("libmmk" in so for so in d["native_so_loaded"])
+
+
+def test_mix_sampler_weights_the_batch_histogram():
+    """The CPU legs' batch-time estimate: per-tile-count mean seconds x the batch's tile counts,
+    unsampled tile counts scaled by encoder FLOPs."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2502_00937_b200 import core
+    spec = core.get_model_spec("llama3.2-11b")
+    dims = bench.image_dims(spec, 32)
+    ms = bench.MixSampler(spec, dims, 1000)
+    assert sum(ms.hist.values()) == 32 and ms.group == 1
+    seen = []
+    for _ in range(len(ms.hist)):
+        t, imgs = ms.next_sample()
+        assert all(core.tile_count(im.shape[1], im.shape[0], spec) == t for im in imgs)
+        seen.append(t)
+        ms.record(t, 2.0 * t)
+    assert sorted(seen) == sorted(ms.hist)
+    total, est = ms.batch_seconds()
+    assert abs(total - sum(c * 2.0 * t for t, c in ms.hist.items())) < 1e-9
+    ms2 = bench.MixSampler(spec, dims, 1000)
+    t, _ = ms2.next_sample()
+    ms2.record(t, 5.0)
+    total2, est2 = ms2.batch_seconds()
+    for u in ms2.hist:
+        assert abs(est2[u] - 5.0 * bench.encoder_flops(spec, [u]) / bench.encoder_flops(spec, [t])) < 1e-9
 
 
 import pytest  # noqa: E402

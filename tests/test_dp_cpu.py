@@ -70,3 +70,42 @@ def test_partition_images_shapes():
     assert partition_images([1], 4) == [[0], [], [], []]
     shards = partition_images([1, 2, 3, 4], 2, costs=[1.0, 5.0, 12.0, 20.0])
     assert sorted(i for s in shards for i in s) == [0, 1, 2, 3]
+
+
+def _release_worker(rank, world, port, q):
+    """A sender that reuses ONE output buffer (a replayed CUDA graph's) calls release() before
+    rewriting it, so every step's rows arrive intact (write-after-read on replay)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rows, width = 64, 8
+    h = Handoff(rank, world, dst=0, depth=3)
+    buf = torch.zeros(rows, width)
+    ok = True
+    for step in range(5):
+        h.release(buf)
+        buf.fill_(float(step))  # the "replay" rewriting the captured output
+        h.send(buf, sizes={1: rows}, width=width)
+        if rank == 0:
+            h.flush()
+            ok &= torch.equal(h.received[1], torch.full((rows, width), float(step)))
+        assert len(h.pending) <= 3
+    h.flush()
+    if rank == 0:
+        q.put(ok)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_release_orders_buffer_reuse_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_release_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    ok = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert ok
