@@ -82,18 +82,18 @@ class DeviceEncoder:
         self.norm_shift = (-mean / std).to(torch.float32).to(dev)
 
     # ------------------------------------------------------------------ layers
-    def _block(self, L, resid, x_buf, qkv_buf, h_buf, cu, n_seq, max_s, aux=None):
+    def _block(self, L, resid, x_buf, qkv_buf, h_buf, cu, n_seq, max_s, aux=None, sum_sq=0.0):
         enc = self.enc
         ops.layernorm(resid, *L["ln1"], enc.norm_eps, out=x_buf)
         ops.gemm(x_buf, L["qkv_w"], ops.EPI_BF16, bias=L["qkv_b"], out=qkv_buf)
-        ops.attention(qkv_buf, cu, n_seq, max_s, enc.heads, enc.head_dim, out=x_buf)
+        ops.attention(qkv_buf, cu, n_seq, max_s, enc.heads, enc.head_dim, out=x_buf, sum_sq_seqlen=sum_sq)
         ops.gemm(x_buf, L["o_w"], ops.EPI_RESID_F32, bias=L["o_b"], out=resid, gate=L["gate_attn"])
         ops.layernorm(resid, *L["ln2"], enc.norm_eps, out=x_buf)
         ops.gemm(x_buf, L["fc1_w"], ops.ACT_EPI[enc.act], bias=L["fc1_b"], out=h_buf)
         ops.gemm(h_buf, L["fc2_w"], ops.EPI_RESID_F32, bias=L["fc2_b"], out=resid, gate=L["gate_ffn"], aux=aux)
 
     def forward(self, patches: torch.Tensor, total_tiles: int, cu_seqlens: torch.Tensor, n_seq: int, max_seqlen: int,
-                tile_image=None, tile_slot=None, image_ar=None, out_alloc=None) -> torch.Tensor:
+                tile_image=None, tile_slot=None, image_ar=None, out_alloc=None, sum_sq_seqlen: float = 0.0) -> torch.Tensor:
         """patches [total_tiles*P, k_pad] bf16 -> packed embeddings for the LLM prefill.
         cu_seqlens int32 [n_seq+1] token offsets of the attention sequences (one per image).
         out_alloc(rows, width) -> bf16 tensor: destination of the packed output, possibly in the
@@ -116,7 +116,7 @@ class DeviceEncoder:
         if enc.family == "clip":
             n_run = enc.layers if enc.out_layer == -1 else enc.layers + 1 + enc.out_layer
             for L in self.layers[:n_run]:
-                self._block(L, resid, x_buf, qkv_buf, h_buf, cu_seqlens, n_seq, max_seqlen)
+                self._block(L, resid, x_buf, qkv_buf, h_buf, cu_seqlens, n_seq, max_seqlen, sum_sq=sum_sq_seqlen)
             # emitted = hidden_states[out_layer] as transformers' CLIPVisionModel numbers them
             # (modeling_clip.py: post_layernorm touches only the pooled CLS, never the sequence)
             drop = 1 if enc.drop_cls else 0
@@ -131,13 +131,13 @@ class DeviceEncoder:
         for i, L in enumerate(self.layers):
             k = enc.capture_after(i)
             aux = inter[k] if k is not None else None
-            self._block(L, resid, x_buf, qkv_buf, h_buf, cu_seqlens, n_seq, max_seqlen, aux=aux)
+            self._block(L, resid, x_buf, qkv_buf, h_buf, cu_seqlens, n_seq, max_seqlen, aux=aux, sum_sq=sum_sq_seqlen)
         # layernorm_post + gated post-tile positional embedding, in place on the fp32 stream
         ops.layernorm(resid, *self.post_ln, enc.norm_eps, out=resid, out_f32=True, tile_add=self.post_tile_scaled,
                       tile_image=tile_image, image_table=image_ar, tile_slot=tile_slot, rows_per_tile=P + 1,
                       slots=self.slots)
         for L in self.global_layers:
-            self._block(L, resid, x_buf, qkv_buf, h_buf, cu_seqlens, n_seq, max_seqlen)
+            self._block(L, resid, x_buf, qkv_buf, h_buf, cu_seqlens, n_seq, max_seqlen, sum_sq=sum_sq_seqlen)
         del x_buf, qkv_buf, h_buf
         if out_alloc is not None:
             return ops.pack_mllama(resid, inter, out=out_alloc(T, d * (1 + len(outs))), peer=True)

@@ -223,14 +223,14 @@ class ImagePathExecutor:
         # attention sequences: all tokens of one image (images never attend to each other)
         seq_len = np.asarray(tiles, np.float64) * (P + 1)
         cu = ops.seq_offsets(plan["tile_off"], n, P + 1)  # device-side: capturable in a CUDA graph
-        ops.set_attention_flops(cu, float(4 * np.sum(seq_len ** 2)))
+        sum_sq = float(np.sum(seq_len ** 2))
         max_s = int(max(tiles)) * (P + 1)
         if enc.family == "mllama":
             tile_image, tile_slot = ops.tile_index(plan["tile_off"], n, total_tiles)
             emb = self.encoder.forward(patches, total_tiles, cu, n, max_s, tile_image, tile_slot, plan["ar_id"],
-                                       out_alloc=out_alloc)
+                                       out_alloc=out_alloc, sum_sq_seqlen=sum_sq)
         else:
-            emb = self.encoder.forward(patches, total_tiles, cu, n, max_s, out_alloc=out_alloc)
+            emb = self.encoder.forward(patches, total_tiles, cu, n, max_s, out_alloc=out_alloc, sum_sq_seqlen=sum_sq)
         return PackedBatch(embeds=emb, tok_offsets=plan["tok_off"], tiles=tiles,
                            image_tokens=[t * spec.tokens_per_tile for t in tiles])
 

@@ -83,6 +83,18 @@ def _need(t, dtype, name):
         raise SpecError(f"{name}: expected a contiguous tensor")
 
 
+def _need_rows(t, dtype, name, min_cols: int | None = None):
+    """A CUDA matrix of ``dtype`` with unit inner stride (row pitch may exceed the width)."""
+    if not isinstance(t, torch.Tensor) or t.dtype != dtype or not t.is_cuda:
+        raise SpecError(f"{name}: expected a CUDA {dtype} tensor, got "
+                        f"{getattr(t, 'dtype', type(t))} on {getattr(t, 'device', '?')}")
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise SpecError(f"{name}: expected a 2-D tensor with unit inner stride, got shape {tuple(t.shape)} "
+                        f"strides {t.stride()}")
+    if min_cols is not None and t.shape[1] < min_cols:
+        raise SpecError(f"{name}: {t.shape[1]} columns < {min_cols}")
+
+
 def tile_plan(w: torch.Tensor, h: torch.Tensor, spec, resize_mode: int | None = None):
     """K0 on device: dict(tiles, tile_off, tok_off, geom, ar_id, bad) (all device tensors)."""
     _need(w, torch.int32, "w")
@@ -145,16 +157,29 @@ def preprocess(src, src_off, w, h, tile_off, geom, n: int, total_tiles: int, spe
 
 def gemm(a: torch.Tensor, b: torch.Tensor, epilogue: int = EPI_BF16, bias=None, out=None, gate: float = 1.0,
          aux=None):
-    """out = epilogue(a @ b.T): a [M, K] bf16, b [N, K] bf16 (nn.Linear weight layout)."""
+    """out = epilogue(a @ b.T): a [M, K] bf16, b [N, K] bf16 (nn.Linear weight layout).  Operands
+    are checked (CUDA, dtype, unit inner stride) before the raw pointers cross the C ABI."""
+    _need_rows(a, torch.bfloat16, "gemm a")
+    _need_rows(b, torch.bfloat16, "gemm b")
     m, k = a.shape
     n = b.shape[0]
     if b.shape[1] != k:
         raise SpecError(f"gemm: K mismatch {a.shape} x {b.shape}")
+    if epilogue not in EPI_NAMES:
+        raise SpecError(f"gemm: unknown epilogue {epilogue}")
     f32_out = epilogue in (EPI_F32, EPI_RESID_F32)
     if out is None:
         if epilogue == EPI_RESID_F32:
             raise SpecError("gemm: RESID_F32 needs the residual tensor as `out`")
         out = torch.empty(m, n, dtype=torch.float32 if f32_out else torch.bfloat16, device=a.device)
+    _need_rows(out, torch.float32 if f32_out else torch.bfloat16, "gemm out", n)
+    if out.shape[0] != m:
+        raise SpecError(f"gemm: out has {out.shape[0]} rows, a {m}")
+    if bias is not None:
+        if bias.dtype != torch.float32 or not bias.is_cuda or not bias.is_contiguous() or bias.numel() != n:
+            raise SpecError(f"gemm: bias must be a contiguous CUDA float32 [{n}] tensor")
+    if aux is not None:
+        _need_rows(aux, torch.bfloat16, "gemm aux", n)
     _t0 = _begin()
     _lib.check(_lib.lib.mmk_gemm_bf16(a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), m, n, k, epilogue,
                                       _p(bias), out.data_ptr(), out.stride(0), float(gate), _p(aux),
@@ -176,27 +201,22 @@ def layernorm(x, gamma, beta, eps: float, out=None, out_f32: bool = False, tile_
     return out
 
 
-_SEQ_FLOPS: dict = {}
-
-
-def set_attention_flops(cu_seqlens, flops_per_head_dim: float):
-    """Register sum(4 * S_i^2) for a cu_seqlens tensor (host-known; avoids a device sync)."""
-    _SEQ_FLOPS[cu_seqlens.data_ptr()] = flops_per_head_dim
-
-
-def _attn_flops(cu_seqlens, heads, head_dim):
-    return _SEQ_FLOPS.get(cu_seqlens.data_ptr(), 0.0) * heads * head_dim
-
-
 _ATTN_WS_BYTES = int(_lib.lib.mmk_attention_workspace_size())
 _ATTN_LAUNCHES = 1 if os.environ.get("MMK_ATTN_SPEC", "1") == "0" else 2  # speculative + gated exact pass
 
 
 def attention(qkv, cu_seqlens, n_seq: int, max_seqlen: int, heads: int, head_dim: int, out=None,
-              scale: float | None = None):
+              scale: float | None = None, sum_sq_seqlen: float = 0.0):
+    """K5 varlen attention over [Q | K | V] rows; ``sum_sq_seqlen`` = sum of S_i^2 over the
+    sequences (host-known; only feeds the roofline log: 4 * sum S^2 * heads * head_dim flops)."""
+    _need_rows(qkv, torch.bfloat16, "qkv", 3 * heads * head_dim)
+    _need(cu_seqlens, torch.int32, "cu_seqlens")
     T = qkv.shape[0]
     if out is None:
         out = torch.empty(T, heads * head_dim, dtype=torch.bfloat16, device=qkv.device)
+    _need_rows(out, torch.bfloat16, "out", heads * head_dim)
+    if out.shape[0] != T:
+        raise SpecError(f"attention: out has {out.shape[0]} rows, qkv {T}")
     if scale is None:
         scale = head_dim ** -0.5
     # per-call workspace (the persistent kernel's work-item counter; stream-ordered by the allocator)
@@ -204,7 +224,7 @@ def attention(qkv, cu_seqlens, n_seq: int, max_seqlen: int, heads: int, head_dim
     _t0 = _begin()
     _lib.check(_lib.lib.mmk_attention_varlen_bf16(qkv.data_ptr(), out.data_ptr(), cu_seqlens.data_ptr(), n_seq,
                                                   max_seqlen, T, heads, head_dim, float(scale), ws.data_ptr(), _s()))
-    _end('attention', _attn_flops(cu_seqlens, heads, head_dim), _t0, launches=_ATTN_LAUNCHES)
+    _end('attention', 4.0 * sum_sq_seqlen * heads * head_dim, _t0, launches=_ATTN_LAUNCHES)
     return out
 
 

@@ -10,8 +10,17 @@ reference's profile JSON schema (profiles.py:268-293) so that ``lmmsim`` autosca
 capacity planning can run on measured numbers.
 
 Encode cost is not linear in tiles (attention is quadratic in an image's tokens), so the
-profile keys on the batch's total tiles measured with the generator's tile mix and
-interpolates piecewise-linearly between measured points.
+profile keeps two measurements: the batch's total tiles with the generator's tile mix
+(piecewise-linear, behind the reference's ``encode_latency(batch_tiles, tp)``), and the cost of
+an image of each tile count inside a full batch (``encode_latency_images``: a batch priced from
+its tile histogram).
+
+TP: the B200 build scales the encoder by data parallelism over images (north_star), not by
+tensor parallelism.  ``measured_tp`` lists the degrees whose latency is known; the export to
+the reference schema writes, for each TP degree of the spec, the DP-equivalent latency — the
+batch split over that many GPUs (``dp_efficiency`` = measured multi-GPU throughput over N x the
+one-GPU throughput, 1.0 when unmeasured) — so a reference simulation whose ``select_sharding``
+picks TP > 1 prices it with what that many B200s achieve on this path.
 """
 
 from __future__ import annotations
@@ -36,6 +45,8 @@ class MeasuredProfile:
     preprocess_floor_ms: float = 0.0
     measured_tp: tuple[int, ...] = (1,)
     meta: dict = field(default_factory=dict)
+    tile_costs: dict = field(default_factory=dict)  # tiles per image -> ms per image inside a batch
+    dp_efficiency: dict = field(default_factory=dict)  # GPUs -> throughput / (GPUs x one-GPU throughput)
 
     def __post_init__(self):
         self.encode_points = sorted((int(t), float(ms)) for t, ms in self.encode_points)
@@ -70,6 +81,29 @@ class MeasuredProfile:
         slope = (hi[1] - lo[1]) / (hi[0] - lo[0])
         return max(0.0, lo[1] + slope * (batch_tiles - lo[0]))
 
+    def encode_latency_images(self, tiles_list, tp: int = 1) -> float:
+        """Measured encode time of a batch priced from its tile histogram (ms): sum over images of
+        the per-image cost of its tile count (super-linear in tiles), over ``tp`` DP GPUs."""
+        if not tiles_list:
+            raise ProfileError("encode batch must contain at least one image")
+        if not self.tile_costs:
+            return self.encode_latency(int(sum(tiles_list)), tp)
+        if tp not in self.dp_gpus():
+            raise ProfileError(f"{tp} GPUs not measured for {self.model.name} (measured: {self.dp_gpus()})")
+        costs = {int(k): float(v) for k, v in self.tile_costs.items()}
+        known = sorted(costs)
+        total = 0.0
+        for t in tiles_list:
+            if t in costs:
+                total += costs[t]
+            else:  # nearest measured tile count, scaled quadratically in tokens
+                k = min(known, key=lambda u: abs(u - t))
+                total += costs[k] * (t / k) ** 2
+        return total / (tp * self.dp_efficiency.get(tp, 1.0))
+
+    def dp_gpus(self) -> list[int]:
+        return sorted({1, *(int(k) for k in self.dp_efficiency)})
+
     def encode_ms_per_tile(self) -> float:
         """Marginal ms per tile at the largest measured batch (throughput regime)."""
         t, ms = self.encode_points[-1]
@@ -80,6 +114,8 @@ class MeasuredProfile:
         return {"model": self.model.name, "encode_points": [list(p) for p in self.encode_points],
                 "preprocess_ms_per_tile": self.preprocess_ms_per_tile,
                 "preprocess_floor_ms": self.preprocess_floor_ms, "measured_tp": list(self.measured_tp),
+                "tile_costs": {str(k): v for k, v in self.tile_costs.items()},
+                "dp_efficiency": {str(k): v for k, v in self.dp_efficiency.items()},
                 "meta": self.meta}
 
     @classmethod
@@ -89,7 +125,9 @@ class MeasuredProfile:
         return cls(model=model, encode_points=[tuple(p) for p in d["encode_points"]],
                    preprocess_ms_per_tile=float(d["preprocess_ms_per_tile"]),
                    preprocess_floor_ms=float(d.get("preprocess_floor_ms", 0.0)),
-                   measured_tp=tuple(d.get("measured_tp", (1,))), meta=dict(d.get("meta", {})))
+                   measured_tp=tuple(d.get("measured_tp", (1,))), meta=dict(d.get("meta", {})),
+                   tile_costs={int(k): float(v) for k, v in d.get("tile_costs", {}).items()},
+                   dp_efficiency={int(k): float(v) for k, v in d.get("dp_efficiency", {}).items()})
 
     def save(self, path) -> None:
         Path(path).write_text(json.dumps(self.to_dict(), indent=2) + "\n")
@@ -101,21 +139,29 @@ class MeasuredProfile:
 
         ``prep_ms_per_tile_core`` is the per-tile cost times the core count the reference divides
         by (so ``preprocess_latency`` returns the measured GPU time for that core count);
-        ``encode_ms_per_tile`` holds the measured marginal ms per tile for each measured TP."""
+        ``encode_ms_per_tile`` holds the measured marginal ms per tile for every TP degree the
+        spec supports, TP > 1 as its DP-equivalent (ms per tile / (tp x dp_efficiency[tp]))."""
         if base.get("model") != self.model.name:
             raise ProfileError(f"base profile is for {base.get('model')}, not {self.model.name}")
         out = dict(base)
         cores = cpu_cores or int(base.get("ref_cpu_cores", 8))
         out["prep_ms_per_tile_core"] = self.preprocess_ms_per_tile * cores
         out["prep_floor_ms"] = self.preprocess_floor_ms
-        out["encode_ms_per_tile"] = {str(tp): self.encode_ms_per_tile() for tp in self.measured_tp}
+        m = self.encode_ms_per_tile()
+        out["encode_ms_per_tile"] = {str(tp): m / (tp * self.dp_efficiency.get(tp, 1.0))
+                                     for tp in self.model.supported_tp_encoder}
+        out["b200_measured"] = {"encode_points": [list(p) for p in self.encode_points],
+                                "tile_costs": {str(k): v for k, v in self.tile_costs.items()},
+                                "tp_semantics": "TP>1 = data parallel over that many B200s (DP-equivalent)",
+                                "dp_efficiency": {str(k): v for k, v in self.dp_efficiency.items()}}
         return out
 
 
 def measure_profile(executor, batch_sizes=(1, 4, 16, 32), warmup: int = 2, iters: int = 5,
-                    seed: int = 0) -> MeasuredProfile:
-    """Time the real image path (CUDA events) on generator-drawn images at several batch
-    sizes; returns the measured profile.  Needs a GPU."""
+                    seed: int = 0, per_count_batch: int = 8) -> MeasuredProfile:
+    """Time the real image path (CUDA events) on generator-drawn images at several batch sizes,
+    and the per-image cost of every tile count inside a batch of ``per_count_batch`` images of
+    that count; returns the measured profile.  Needs a GPU."""
     import numpy as np
     import torch
 
@@ -127,9 +173,8 @@ def measure_profile(executor, batch_sizes=(1, 4, 16, 32), warmup: int = 2, iters
     cfg = workload.GeneratorConfig(model=spec, base_rate=50.0, image_request_fraction=1.0, seed=seed)
     dims = workload.image_dims_of(workload.generate(cfg, 20_000.0))
     rng = np.random.default_rng(seed)
-    points, prep = [], []
-    for b in batch_sizes:
-        d = dims[:b]
+
+    def time_batch(d):
         imgs = [rng.integers(0, 256, (h, w, 3), dtype=np.uint8) for w, h in d]
         staged = stage_images(imgs, executor.device)
         for _ in range(warmup):
@@ -144,11 +189,27 @@ def measure_profile(executor, batch_sizes=(1, 4, 16, 32), warmup: int = 2, iters
         e.record()
         ops.LOG = None
         torch.cuda.synchronize()
-        tiles = sum(tile_count(w, h, spec) for w, h in d)
-        points.append((tiles, s.elapsed_time(e) / iters))
         k = log.summary()
         prep_ms = sum(k.get(n, {}).get("ms", 0.0) for n in ("tile_plan", "preprocess")) / iters
+        return s.elapsed_time(e) / iters, prep_ms
+
+    points, prep = [], []
+    for b in batch_sizes:
+        d = dims[:b]
+        ms, prep_ms = time_batch(d)
+        tiles = sum(tile_count(w, h, spec) for w, h in d)
+        points.append((tiles, ms))
         prep.append(prep_ms / tiles)
+    tile_costs = {}
+    by_count: dict = {}
+    for w, h in dims:
+        by_count.setdefault(tile_count(w, h, spec), []).append((w, h))
+    for t in sorted(by_count):
+        d = (by_count[t] * per_count_batch)[:per_count_batch]
+        ms, _ = time_batch(d)
+        tile_costs[t] = ms / len(d)
     return MeasuredProfile(model=spec, encode_points=points, preprocess_ms_per_tile=float(np.mean(prep)),
+                           tile_costs=tile_costs,
                            meta={"device": torch.cuda.get_device_name(), "batch_sizes": list(batch_sizes),
-                                 "iters": iters, "tile_mix": "reference generator, seed %d" % seed})
+                                 "per_count_batch": per_count_batch, "iters": iters,
+                                 "tile_mix": "reference generator, seed %d" % seed})

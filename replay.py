@@ -31,7 +31,11 @@ def main():
     ap.add_argument("--burst-mult", type=float, default=3.0)
     ap.add_argument("--max-batch", type=int, default=8)
     ap.add_argument("--scheduler", default="slo_priority", choices=["fifo", "slo_priority"])
-    ap.add_argument("--ms-per-tile", type=float, default=5.0, help="routing cost model (measured ~4.9 on B200)")
+    ap.add_argument("--profile", default=None,
+                    help="measured profile for the router's cost model (default profiles/measured_<model>.json; "
+                         "measured on this GPU at start-up when absent)")
+    ap.add_argument("--ms-per-tile", type=float, default=None,
+                    help="override: a linear routing cost model instead of the measured profile")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--connector", action="store_true", help="apply the LLM-side projector on rank 0 as shards land")
     ap.add_argument("--handoff", default="peer", choices=["peer", "nccl"],
@@ -83,8 +87,27 @@ def main():
     if args.connector and rank == 0:
         from paper_2502_00937_b200.connector import Projector
         connector = Projector(spec)
+    # the router's cost model: the B200-measured encode latency (MeasuredProfile, the reference's
+    # encode_latency seam, piecewise linear over batch tiles) — every rank loads / measures the
+    # same profile so their deterministic routing agrees
+    from paper_2502_00937_b200.profiles import MeasuredProfile, measure_profile
+    if args.ms_per_tile is not None:
+        cost_ms, cost_src = (lambda tiles: args.ms_per_tile * tiles), f"linear {args.ms_per_tile} ms/tile"
+    else:
+        path = args.profile or os.path.join(ROOT, "profiles", f"measured_{spec.name}.json")
+        if os.path.exists(path):
+            prof = MeasuredProfile.from_dict(json.loads(open(path).read()), spec)
+            cost_src = f"measured profile {os.path.relpath(path, ROOT)}"
+        else:
+            prof = measure_profile(ex, batch_sizes=(1, 4, 16), iters=3, per_count_batch=4)
+            if world > 1:  # one profile for every rank's router
+                obj = [prof.to_dict()]
+                dist.broadcast_object_list(obj, src=0)
+                prof = MeasuredProfile.from_dict(obj[0], spec)
+            cost_src = "measured at start-up"
+        cost_ms = lambda tiles: prof.encode_latency(max(1, tiles), 1)  # noqa: E731
     svc = ImagePathService(spec, ex, rank=rank, world=world, policies=pol, max_batch={"encode": args.max_batch},
-                           cost_ms=lambda tiles: args.ms_per_tile * tiles, ttft_slo_ms=2000.0, connector=connector)
+                           cost_ms=cost_ms, ttft_slo_ms=2000.0, connector=connector)
     chan = None
     digests = {}
 
@@ -118,7 +141,8 @@ def main():
                 "trace": {"generator": "reference workload.generate", "seed": args.seed, "duration_s": args.duration_s,
                           "rate_req_s": args.rate * world, "burst": [burst.start_ms, burst.duration_ms, burst.rate_multiplier],
                           "images_per_request": IMAGES_PER_REQUEST, "requests": len(reqs), "images": n_img},
-                "batcher": {"router": "least_pending", "scheduler": args.scheduler, "max_batch_encode": args.max_batch},
+                "batcher": {"router": "least_pending", "scheduler": args.scheduler, "max_batch_encode": args.max_batch,
+                            "router_cost_model": cost_src},
                 "connector": "mllama multi_modal_projector on rank 0" if args.connector else None,
                 "handoff": (args.handoff if world > 1 else None),
                 "handoff_shards": (dict(chan.counts) if chan is not None else None),

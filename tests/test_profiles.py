@@ -50,7 +50,9 @@ def test_roundtrip_and_reference_export(tmp_path):
         MeasuredProfile.from_dict(p.to_dict(), core.get_model_spec("internvl-26b"))
     base = json.loads((GOLD / "profile_llama.json").read_text())
     ref = p.to_reference_profile(base)
-    assert ref["encode_ms_per_tile"] == {"1": pytest.approx(700.0 / 64)}
+    # every TP degree of the spec: TP-1 measured, TP > 1 as its data-parallel equivalent
+    assert ref["encode_ms_per_tile"] == {"1": pytest.approx(700.0 / 64), "2": pytest.approx(350.0 / 64),
+                                         "4": pytest.approx(175.0 / 64), "8": pytest.approx(87.5 / 64)}
     assert ref["prefill_self_ms_per_token"] == base["prefill_self_ms_per_token"]
     # the reference's own loader (authoring container only) prices stages with the measured constants
     if not Path("/root/reference/pkg/src").exists():
@@ -60,4 +62,44 @@ def test_roundtrip_and_reference_export(tmp_path):
     from lmmsim import profiles as rprofiles
     rp = rprofiles.LatencyProfile.from_dict(ref, rcore.get_model_spec("llama3.2-11b"))
     assert rp.encode_latency(64, 1) == pytest.approx(700.0)
+    assert rp.encode_latency(64, 4) == pytest.approx(175.0)  # select_sharding picking TP-4 no longer fails
     assert rp.preprocess_latency(100, base["ref_cpu_cores"]) == pytest.approx(1.0)
+
+
+def test_batch_priced_from_its_tile_histogram():
+    """encode_latency_images: per-image cost of each tile count (super-linear in tiles), DP over
+    GPUs with the measured efficiency; unknown tile counts scale quadratically in tokens."""
+    p = MeasuredProfile(model=LLAMA, encode_points=[(8, 100.0)], preprocess_ms_per_tile=0.01,
+                        tile_costs={1: 3.0, 2: 8.0, 4: 20.0}, dp_efficiency={2: 0.9})
+    assert p.encode_latency_images([1, 1, 2, 4]) == pytest.approx(34.0)
+    assert p.encode_latency_images([3]) == pytest.approx(8.0 * (3 / 2) ** 2)  # nearest measured: 2 (tie -> lower)
+    assert p.encode_latency_images([4, 4], tp=2) == pytest.approx(40.0 / 1.8)
+    with pytest.raises(ProfileError):
+        p.encode_latency_images([1], tp=4)
+    with pytest.raises(ProfileError):
+        p.encode_latency_images([])
+    q = MeasuredProfile.from_dict(json.loads(json.dumps(p.to_dict())), LLAMA)
+    assert q.tile_costs == p.tile_costs and q.dp_efficiency == p.dp_efficiency
+
+
+MEASURED = Path(__file__).resolve().parent.parent / "profiles" / "measured_llama3.2-11b.reference.json"
+
+
+@pytest.mark.skipif(not MEASURED.exists(), reason="no B200-measured profile committed")
+def test_committed_b200_profile_loads_in_the_reference():
+    """The B200-measured profile (scripts/measure_profile.py on a B200) in the reference schema,
+    loaded by the reference's own LatencyProfile.from_dict (profiles.py:299-326)."""
+    ref = json.loads(MEASURED.read_text())
+    mp = MeasuredProfile.from_dict(json.loads((MEASURED.parent / "measured_llama3.2-11b.json").read_text()), LLAMA)
+    assert len(mp.encode_points) >= 3 and set(mp.tile_costs) >= {1, 2, 4}
+    assert mp.tile_costs[4] > 2 * mp.tile_costs[2] > 0  # super-linear in tiles
+    if not Path("/root/reference/pkg/src").exists():
+        pytest.skip("reference not mounted")
+    sys.path.insert(0, "/root/reference/pkg/src")
+    from lmmsim import core as rcore
+    from lmmsim import profiles as rprofiles
+    rp = rprofiles.LatencyProfile.from_dict(ref, rcore.get_model_spec("llama3.2-11b"))
+    t, ms = mp.encode_points[-1]
+    assert rp.encode_latency(t, 1) == pytest.approx(ms, rel=1e-6)
+    for tp in (2, 4, 8):
+        assert rp.encode_latency(t, tp) < rp.encode_latency(t, 1)
