@@ -50,8 +50,16 @@ __device__ long long g_attn_trace[3][64][8];
 constexpr int kTcBQ = 128;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
+// Row sums of P on the tensor core (hd 80): one more TS-MMA per 16-key step, O_t(:, HD) += P_t x ones,
+// so the softmax warps drop their FADD2 sums and l is exactly the sum of the bf16 P the PV used.
+#ifndef MMK_ATTN_LSUM
+#define MMK_ATTN_LSUM 0
+#endif
+
 template <int HD, int BKV, int NQ>
 struct TcAttnCfg {
+  static constexpr bool kLSum = MMK_ATTN_LSUM && HD == 80;   // l accumulated by the tensor core
+  static constexpr int kOCols = HD + (kLSum ? 16 : 0);       // O_t columns (+ the l block)
   static constexpr bool kRem = (HD % 64) != 0;               // has a 16-wide remainder block
   static constexpr int kQMain = kTcBQ * 64 * 2;              // Q tile: 128 rows x 64 cols
   static constexpr int kQBytes = kQMain + (kRem ? kTcBQ * 16 * 2 : 0);
@@ -61,15 +69,16 @@ struct TcAttnCfg {
   static constexpr int kQOff = 0;
   static constexpr int kKVOff = NQ * kQBytes;
   static constexpr int kStageBytes = 2 * kKVBytes;           // K then V
-  static constexpr int kBarOff = kKVOff + STAGES * kStageBytes;
+  static constexpr int kOnesOff = kKVOff + STAGES * kStageBytes;  // 16 keys x 32 B of ones (kLSum)
+  static constexpr int kBarOff = kOnesOff + (kLSum ? 512 : 0);
   static constexpr int kSmem = kBarOff + 256 + 1024;
   static constexpr int kThreads = 32 * (5 * NQ + 1);  // NQ softmax warpgroups, TMA warp, NQ MMA warps
-  static constexpr int kOBase = NQ * BKV;                    // TMEM column of O_0 (O_t: + t*HD)
+  static constexpr int kOBase = NQ * BKV;                    // TMEM column of O_0 (O_t: + t*kOCols)
   // P_t (bf16 pairs) in its own columns when S + O + P fit 512, else aliased onto S_t (then S_t(j+1)
   // is issued only after PV_t(j) has retired, instead of as soon as S_t(j) is in registers)
   static constexpr int kPStrideSep = (BKV / 2 + 31) / 32 * 32;
-  static constexpr bool kAlias = (kOBase + NQ * HD + 31) / 32 * 32 + (NQ - 1) * kPStrideSep + BKV / 2 > 512;
-  static constexpr int kPBase = kAlias ? 0 : (kOBase + NQ * HD + 31) / 32 * 32;  // P_t: + t*kPStride
+  static constexpr bool kAlias = (kOBase + NQ * kOCols + 31) / 32 * 32 + (NQ - 1) * kPStrideSep + BKV / 2 > 512;
+  static constexpr int kPBase = kAlias ? 0 : (kOBase + NQ * kOCols + 31) / 32 * 32;  // P_t: + t*kPStride
   static constexpr int kPStride = kAlias ? BKV : kPStrideSep;
   static_assert(kPBase + (NQ - 1) * kPStride + BKV / 2 <= 512, "TMEM overflow: S + O + P > 512 columns");
   static_assert(BKV % 16 == 0, "key tile");
@@ -141,8 +150,16 @@ MMK_DEV void issue_s(uint32_t s_tm, uint32_t q_addr, uint32_t k_addr) {
 
 // O_t (+)= P_t V for one KV tile: P_t from TMEM (bf16 pairs, 8 columns per 16 keys) as the A
 // operand, V the MN-major B operand (8-row K groups at 128 B main / 32 B remainder per row).
+// The constant B operand of the row-sum MMA: 16 keys x 16 columns, MN-major, 32-byte rows.  Both
+// 16-byte halves of a row are (1, 0, ..., 0), so whatever the 32B swizzle does to a row's halves,
+// columns 0 and 8 of the result hold the row sum of P.
+MMK_DEV void init_ones_tile(uint8_t* p) {
+  uint32_t* w = reinterpret_cast<uint32_t*>(p);
+  for (int i = 0; i < 128; ++i) w[i] = (i & 3) == 0 ? 0x3F80u : 0u;  // bf16 1.0 in the low half of word 0 of each 16 B
+}
+
 template <int HD, int BKV, int NQ>
-MMK_DEV void issue_pv(uint32_t o_tm, uint32_t p_tm, uint32_t v_addr, bool first) {
+MMK_DEV void issue_pv(uint32_t o_tm, uint32_t p_tm, uint32_t v_addr, bool first, uint32_t ones_addr = 0) {
   using C = TcAttnCfg<HD, BKV, NQ>;
   constexpr uint32_t idesc_pv_main = umma_idesc_bf16_f32(kTcBQ, 64) | (1u << 16);  // B (V) MN-major
   constexpr uint32_t idesc_pv_rem = umma_idesc_bf16_f32(kTcBQ, 16) | (1u << 16);
@@ -154,6 +171,7 @@ MMK_DEV void issue_pv(uint32_t o_tm, uint32_t p_tm, uint32_t v_addr, bool first)
     const uint32_t acc = (!first || k > 0) ? 1u : 0u;
     umma_bf16_ts(o_tm, p_tm + 8 * k, vd_main + kVStepMain * k, idesc_pv_main, acc);
     if (C::kRem) umma_bf16_ts(o_tm + 64, p_tm + 8 * k, vd_rem + kVStepRem * k, idesc_pv_rem, acc);
+    if constexpr (C::kLSum) umma_bf16_ts(o_tm + HD, p_tm + 8 * k, umma_desc_sw32_kmajor(ones_addr), idesc_pv_rem, acc);
   }
 }
 
@@ -229,7 +247,7 @@ MMK_DEV void softmax_tile(uint32_t s_tm, uint32_t o_tm, uint32_t p_tm, uint64_t*
     tc_fence_after();
     uint32_t o[16];
 #pragma unroll
-    for (int c = 0; c < HD / 16; ++c) {
+    for (int c = 0; c < TcAttnCfg<HD, BKV, NQ>::kOCols / 16; ++c) {  // with kLSum also rescales l
       tmem_ld_32x32b_x16(o_tm + 16 * c, o);
       tmem_ld_wait();
 #pragma unroll
@@ -260,7 +278,9 @@ MMK_DEV void softmax_tile(uint32_t s_tm, uint32_t o_tm, uint32_t p_tm, uint64_t*
       e.x = fast_exp2(x.x);
       e.y = fast_exp2(x.y);
     }
-    if (i & 1) sb = __fadd2_rn(sb, e); else sa = __fadd2_rn(sa, e);
+    if constexpr (!TcAttnCfg<HD, BKV, NQ>::kLSum) {
+      if (i & 1) sb = __fadd2_rn(sb, e); else sa = __fadd2_rn(sa, e);
+    }
     p[i] = pack_bf16x2(e.x, e.y);
   };
   if (pipelined) {
@@ -288,12 +308,19 @@ MMK_DEV void softmax_tile(uint32_t s_tm, uint32_t o_tm, uint32_t p_tm, uint64_t*
       }
     }
   }
-  float sum = (sa.x + sa.y) + (sb.x + sb.y);
-  if constexpr (SPEC) {
-    if (pm > 126.f) sum = INFINITY;  // wrapped polynomial: route the row to the exact pass
+  if constexpr (TcAttnCfg<HD, BKV, NQ>::kLSum) {
+    // l lives in O_t(:, HD) (tensor-core row sum); the register l only carries the wrap flag
+    if constexpr (SPEC) {
+      if (pm > 126.f) l = INFINITY;  // wrapped polynomial: route the row to the exact pass
+    }
+  } else {
+    float sum = (sa.x + sa.y) + (sb.x + sb.y);
+    if constexpr (SPEC) {
+      if (pm > 126.f) sum = INFINITY;  // wrapped polynomial: route the row to the exact pass
+    }
+    l = l * corr + sum;
   }
   if (trace) { TR(t, j, 3) }
-  l = l * corr + sum;
   // P_t -> TMEM (the previous PV_t must have finished reading the buffer; at the first tile of an
   // item the previous item's last PV retired before its output was read)
   if (!first) mbar_wait(pv_done, (g - 1) & 1);
@@ -318,6 +345,20 @@ MMK_DEV void softmax_tile(uint32_t s_tm, uint32_t o_tm, uint32_t p_tm, uint64_t*
 constexpr float kSpecLimit = 1.2676506e30f;  // 2^100
 MMK_DEV void flag_overflow(float l, int* flag) {
   if (!(l <= kSpecLimit)) *reinterpret_cast<volatile int*>(flag) = 1;  // also catches inf / NaN
+}
+
+// The row's softmax denominator: with kLSum the tensor core's sum in O_t(:, HD) (the register l
+// only carries the speculative pass's wrap flag, +inf), else the register sum.
+template <int HD, int BKV, int NQ>
+MMK_DEV float final_l(uint32_t o_tm, float l) {
+  if constexpr (TcAttnCfg<HD, BKV, NQ>::kLSum) {
+    uint32_t r[4];
+    tmem_ld_32x32b_x4(o_tm + HD, r);
+    tmem_ld_wait();
+    return l == INFINITY ? INFINITY : __uint_as_float(r[0]);
+  } else {
+    return l;
+  }
 }
 
 // O_t / l -> bf16 output row (16 columns per TMEM load, two 16-byte stores).
@@ -396,6 +437,10 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
     fence_barrier_init();
   }
   if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
+  if (C::kLSum && warp == kTmaWarp) {
+    if (lane == 0) init_ones_tile(smem + C::kOnesOff);
+    fence_proxy_async();  // generic-proxy writes read by the MMA (async proxy)
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -437,7 +482,7 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
     const int t = static_cast<int>(warp) - kMmaWarp;
     if (t < n_qt) {
       const uint32_t s_tm = tmem + t * BKV;
-      const uint32_t o_tm = tmem + C::kOBase + t * HD;
+      const uint32_t o_tm = tmem + C::kOBase + t * C::kOCols;
       const uint32_t p_tm = tmem + C::kPBase + t * C::kPStride;
       const uint32_t q_addr = smem_u32(tile_ptr(C::kQOff + t * C::kQBytes));
       mbar_wait(q_full, 0);
@@ -473,7 +518,7 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
           if (t < 2) { TR(2, j - 1, 3 + t) }
           const uint32_t v_addr = smem_u32(tile_ptr(C::kKVOff + pst * C::kStageBytes + C::kKVBytes));
           if (elect_one()) {
-            issue_pv<HD, BKV, NQ>(o_tm, p_tm, v_addr, j == 1);
+            issue_pv<HD, BKV, NQ>(o_tm, p_tm, v_addr, j == 1, smem_u32(smem + C::kOnesOff));
             umma_commit(&pv_done[t]);
             umma_commit(&kv_empty[pst]);  // this tile is done with K(j-1), V(j-1)
           }
@@ -489,7 +534,7 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
     const uint32_t q4 = warp & 3;            // lane quarter
     const uint32_t lane_base = (q4 * 32u) << 16;
     const uint32_t s_tm = tmem + t * BKV + lane_base;
-    const uint32_t o_tm = tmem + C::kOBase + t * HD + lane_base;
+    const uint32_t o_tm = tmem + C::kOBase + t * C::kOCols + lane_base;
     const int row = q0 + t * kTcBQ + q4 * 32 + lane;  // query row within the sequence
     if (t < n_qt) {
       const uint32_t p_tm = tmem + C::kPBase + t * C::kPStride + lane_base;
@@ -500,6 +545,7 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
                                         j);
       mbar_wait(&pv_done[t], (nkv - 1) & 1);
       tc_fence_after();
+      l = final_l<HD, BKV, NQ>(o_tm, l);
       if constexpr (SPEC) flag_overflow(l, overflow_flag);
       store_o<HD>(o_tm, l, out + static_cast<int64_t>(s_begin + row) * d_model + head * HD, row < len);
     }
@@ -537,7 +583,8 @@ struct TcPersistLayout {
   static constexpr int kQSlotBytes = NQ * C::kQBytes;
   static constexpr int kQOff = 0;                          // two Q slots
   static constexpr int kKVOff = 2 * kQSlotBytes;
-  static constexpr int kBarOff = kKVOff + C::STAGES * C::kStageBytes;
+  static constexpr int kOnesOff = kKVOff + C::STAGES * C::kStageBytes;  // row-sum B operand (kLSum)
+  static constexpr int kBarOff = kOnesOff + (C::kLSum ? 512 : 0);
   // longest-first schedule (n_seq <= kMaxSched): lengths, sorted order, item prefix
   static constexpr int kSchedOff = kBarOff + 512;
   static constexpr int kSchedBytes = (3 * kMaxSched + 1) * 4;
@@ -618,6 +665,10 @@ attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_co
     fence_barrier_init();
   }
   if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
+  if (C::kLSum && warp == kTmaWarp) {
+    if (lane == 0) init_ones_tile(smem + Lay::kOnesOff);
+    fence_proxy_async();  // generic-proxy writes read by the MMA (async proxy)
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -739,7 +790,7 @@ attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_co
     // ---------------------------------------------------------------- MMA issuers
     const int t = static_cast<int>(warp) - kMmaWarp;
     const uint32_t s_tm = tmem + t * BKV;
-    const uint32_t o_tm = tmem + C::kOBase + t * HD;
+    const uint32_t o_tm = tmem + C::kOBase + t * C::kOCols;
     const uint32_t p_tm = tmem + C::kPBase + t * C::kPStride;
     uint32_t kv = 0, qi = 0, g = 0, oi = 0, k = 0;
     for (;;) {
@@ -793,7 +844,7 @@ attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_co
           tc_fence_after();
           const uint32_t v_addr = smem_u32(tile_ptr(Lay::kKVOff + pst * C::kStageBytes + C::kKVBytes));
           if (elect_one()) {
-            issue_pv<HD, BKV, NQ>(o_tm, p_tm, v_addr, j == 1);
+            issue_pv<HD, BKV, NQ>(o_tm, p_tm, v_addr, j == 1, smem_u32(smem + Lay::kOnesOff));
             umma_commit(&pv_done[t]);
             umma_commit(&kv_empty[pst]);
           }
@@ -811,7 +862,7 @@ attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_co
     const uint32_t q4 = warp & 3;
     const uint32_t lane_base = (q4 * 32u) << 16;
     const uint32_t s_tm = tmem + t * BKV + lane_base;
-    const uint32_t o_tm = tmem + C::kOBase + t * HD + lane_base;
+    const uint32_t o_tm = tmem + C::kOBase + t * C::kOCols + lane_base;
     const uint32_t p_tm = tmem + C::kPBase + t * C::kPStride + lane_base;
     uint32_t g = 0, k = 0;
     for (;;) {
@@ -825,6 +876,7 @@ attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       g += it.nkv;
       mbar_wait(&pv_done[t], (g - 1) & 1);
       tc_fence_after();
+      l = final_l<HD, BKV, NQ>(o_tm, l);
       if constexpr (SPEC) flag_overflow(l, overflow_flag);
       const int row = it.q0 + t * kTcBQ + q4 * 32 + lane;
       store_o<HD>(o_tm, l, out + static_cast<int64_t>(it.s_begin + row) * d_model + it.head * HD, row < it.len);
