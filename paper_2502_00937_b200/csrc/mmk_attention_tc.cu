@@ -55,6 +55,12 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef MMK_ATTN_LSUM
 #define MMK_ATTN_LSUM 0
 #endif
+// Split softmax (needs LSUM): two warps per TMEM lane quarter, each owning half of a KV tile's
+// keys, so every SM sub-partition runs twice as many softmax warps; with the tensor-core row sums
+// and the speculative max the halves only meet at an item's first tile (row max via shared memory).
+#ifndef MMK_ATTN_SPLIT
+#define MMK_ATTN_SPLIT 0
+#endif
 
 template <int HD, int BKV, int NQ>
 struct TcAttnCfg {
@@ -72,7 +78,10 @@ struct TcAttnCfg {
   static constexpr int kOnesOff = kKVOff + STAGES * kStageBytes;  // 16 keys x 32 B of ones (kLSum)
   static constexpr int kBarOff = kOnesOff + (kLSum ? 512 : 0);
   static constexpr int kSmem = kBarOff + 256 + 1024;
-  static constexpr int kThreads = 32 * (5 * NQ + 1);  // NQ softmax warpgroups, TMA warp, NQ MMA warps
+  static constexpr bool kSplit = MMK_ATTN_SPLIT && kLSum;
+  static constexpr int kHalves = kSplit ? 2 : 1;
+  static constexpr int kSoftmaxWarps = 4 * NQ * kHalves;
+  static constexpr int kThreads = 32 * (kSoftmaxWarps + 1 + NQ);  // softmax warps, TMA warp, NQ MMA warps
   static constexpr int kOBase = NQ * BKV;                    // TMEM column of O_0 (O_t: + t*kOCols)
   // P_t (bf16 pairs) in its own columns when S + O + P fit 512, else aliased onto S_t (then S_t(j+1)
   // is issued only after PV_t(j) has retired, instead of as soon as S_t(j) is in registers)
@@ -347,6 +356,107 @@ MMK_DEV void flag_overflow(float l, int* flag) {
   if (!(l <= kSpecLimit)) *reinterpret_cast<volatile int*>(flag) = 1;  // also catches inf / NaN
 }
 
+// Split form of softmax_tile (C::kSplit): this warp owns keys [h*KH, (h+1)*KH) of the tile for its
+// 32 rows; the partner warp (same rows, other half) meets it only where a row max is computed
+// (an item's first tile with SPEC, every tile without), through `red` [2][32] in shared memory and
+// a 64-thread named barrier.  l is summed by the tensor core (kLSum); half 0 rescales O.
+template <int HD, int BKV, int NQ, bool SPEC>
+MMK_DEV void softmax_tile_split(uint32_t s_tm, uint32_t o_tm, uint32_t p_tm, uint64_t* s_full, uint64_t* s_free,
+                                uint64_t* pv_done, uint64_t* p_full, uint32_t g, bool first, int valid,
+                                float scale_log2, float& m_used, float& l, uint32_t lane, int h, float* red,
+                                uint32_t bar_id) {
+  constexpr int KH = BKV / 2;
+  static_assert(KH % 16 == 0 && KH <= 64, "half tile");
+  mbar_wait(s_full, g & 1);
+  tc_fence_after();
+  uint32_t r[KH];
+  const uint32_t sc = s_tm + h * KH;
+  tmem_ld_32x32b_x32(sc, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+  if constexpr (KH > 32) tmem_ld_32x32b_x16(sc + 32, *reinterpret_cast<uint32_t(*)[16]>(&r[32]));
+  tmem_ld_wait();
+  reg_fence<KH>(r);
+  tc_fence_before();
+  __syncwarp();
+  if (lane == 0) mbar_arrive(s_free);
+  const int vh = valid - h * KH;  // keys of this half inside the sequence
+  if (vh < KH) {
+#pragma unroll
+    for (int i = 0; i < KH; ++i)
+      if (i >= vh) r[i] = __float_as_uint(-INFINITY);
+  }
+  float m_new = m_used, corr = 1.f;
+  if (!SPEC || first) {
+    float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+    for (int i = 0; i < KH; i += 8)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) m4[u] = fmax3(m4[u], __uint_as_float(r[i + 2 * u]), __uint_as_float(r[i + 2 * u + 1]));
+    float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+    red[h * 32 + lane] = mx;
+    named_bar_sync(bar_id, 64);
+    mx = fmaxf(mx, red[(h ^ 1) * 32 + lane]) * scale_log2;
+    named_bar_sync(bar_id, 64);  // both read before the next exchange overwrites
+    if (mx > m_used + kRescaleThreshold) {
+      m_new = mx;
+      corr = fast_exp2(m_used - m_new);
+    }
+  }
+  if (!SPEC && !first && h == 0 && warp_any(corr != 1.f)) {
+    mbar_wait(pv_done, (g - 1) & 1);
+    tc_fence_after();
+    uint32_t o[16];
+#pragma unroll
+    for (int c = 0; c < TcAttnCfg<HD, BKV, NQ>::kOCols / 16; ++c) {
+      tmem_ld_32x32b_x16(o_tm + 16 * c, o);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * corr);
+      tmem_st_32x32b_x16(o_tm + 16 * c, o);
+    }
+    tmem_st_wait();
+  }
+  m_used = m_new;
+  const float2 sc2 = make_float2(scale_log2, scale_log2);
+  const float2 nm2 = make_float2(-m_new, -m_new);
+  float pm = -INFINITY;
+  uint32_t p[KH / 2];
+#pragma unroll
+  for (int i = 0; i < KH / 2; ++i) {
+    float2 e;
+    if (vh <= 2 * i) {  // pairs past the sequence end (last tile, uniform)
+      e = make_float2(0.f, 0.f);
+    } else {
+      const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), sc2, nm2);
+      if ((i & 7) < (SPEC ? MMK_POLY8_SPEC : MMK_POLY8)) {
+        if constexpr (SPEC) pm = fmax3(pm, x.x, x.y);
+        e = exp2_poly2(x);
+      } else {
+        e.x = fast_exp2(x.x);
+        e.y = fast_exp2(x.y);
+      }
+    }
+    p[i] = pack_bf16x2(e.x, e.y);
+  }
+  if constexpr (SPEC) {
+    if (pm > 126.f) l = INFINITY;
+  }
+  if (!first) mbar_wait(pv_done, (g - 1) & 1);
+  tc_fence_after();
+  const uint32_t pc = p_tm + h * (KH / 2);
+  if constexpr (KH / 2 == 32) {
+    tmem_st_32x32b_x32(pc, *reinterpret_cast<const uint32_t(*)[32]>(&p[0]));
+  } else {
+    static_assert(KH / 2 == 24 || KH / 2 == 16 || KH / 2 == 8, "P half");
+    if constexpr (KH / 2 >= 16) tmem_st_32x32b_x16(pc, *reinterpret_cast<const uint32_t(*)[16]>(&p[0]));
+    if constexpr (KH / 2 == 24 || KH / 2 == 8)
+      tmem_st_32x32b_x8(pc + (KH / 2 >= 16 ? 16 : 0), *reinterpret_cast<const uint32_t(*)[8]>(&p[KH / 2 >= 16 ? 16 : 0]));
+  }
+  tmem_st_wait();
+  tc_fence_before();
+  __syncwarp();
+  if (lane == 0) mbar_arrive(p_full);
+}
+
 // The row's softmax denominator: with kLSum the tensor core's sum in O_t(:, HD) (the register l
 // only carries the speculative pass's wrap flag, +inf), else the register sum.
 template <int HD, int BKV, int NQ>
@@ -381,13 +491,14 @@ MMK_DEV void store_o(uint32_t o_tm, float l, __nv_bfloat16* go, bool row_ok) {
 }
 
 template <int HD, int BKV, int NQ, bool SPEC>
-__global__ void __maxnreg__(NQ == 2 ? 168 : 128)
+__global__ void __maxnreg__(MMK_ATTN_SPLIT && HD == 80 ? 96 : (NQ == 2 ? 168 : 128))
 attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_q_rem,
             const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_kv_rem,
             __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ cu_seqlens, int heads, float scale_log2,
             int* __restrict__ overflow_flag) {
   using C = TcAttnCfg<HD, BKV, NQ>;
-  constexpr int kTmaWarp = 4 * NQ, kMmaWarp = 4 * NQ + 1;  // MMA warp of query tile t: kMmaWarp + t
+  constexpr int kTmaWarp = C::kSoftmaxWarps, kMmaWarp = C::kSoftmaxWarps + 1;  // MMA warp of tile t: kMmaWarp + t
+  __shared__ float s_red[C::kSplit ? 4 * NQ * 64 : 1];  // split softmax: row-max exchange
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
@@ -430,8 +541,8 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
     }
     for (int t = 0; t < NQ; ++t) {
       mbar_init(&s_full[t], 1);
-      mbar_init(&s_free[t], 4);  // one arrive per softmax warp
-      mbar_init(&p_full[t], 4);
+      mbar_init(&s_free[t], 4 * C::kHalves);  // one arrive per softmax warp
+      mbar_init(&p_full[t], 4 * C::kHalves);
       mbar_init(&pv_done[t], 1);
     }
     fence_barrier_init();
@@ -530,7 +641,8 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
     }
   } else {
     // ---------------------------------------------------------------- softmax warpgroups
-    const int t = warp >> 2;                 // query tile
+    const int t = warp / (4 * C::kHalves);   // query tile
+    const int h = (warp >> 2) % C::kHalves;  // key half (split softmax)
     const uint32_t q4 = warp & 3;            // lane quarter
     const uint32_t lane_base = (q4 * 32u) << 16;
     const uint32_t s_tm = tmem + t * BKV + lane_base;
@@ -539,15 +651,25 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
     if (t < n_qt) {
       const uint32_t p_tm = tmem + C::kPBase + t * C::kPStride + lane_base;
       float m_used = -INFINITY, l = 0.f;
-      for (int j = 0; j < nkv; ++j)
-        softmax_tile<HD, BKV, NQ, SPEC>(s_tm, o_tm, p_tm, &s_full[t], &s_free[t], &pv_done[t], &p_full[t], j, j == 0,
-                                        len - j * BKV, scale_log2, m_used, l, lane, q4 == 0 && lane == 0 && t < 2, t,
-                                        j);
+      for (int j = 0; j < nkv; ++j) {
+        if constexpr (C::kSplit)
+          softmax_tile_split<HD, BKV, NQ, SPEC>(s_tm, o_tm, p_tm, &s_full[t], &s_free[t], &pv_done[t], &p_full[t], j,
+                                                j == 0, len - j * BKV, scale_log2, m_used, l, lane, h,
+                                                s_red + (t * 4 + q4) * 64, 1 + t * 4 + q4);
+        else
+          softmax_tile<HD, BKV, NQ, SPEC>(s_tm, o_tm, p_tm, &s_full[t], &s_free[t], &pv_done[t], &p_full[t], j, j == 0,
+                                          len - j * BKV, scale_log2, m_used, l, lane, q4 == 0 && lane == 0 && t < 2, t,
+                                          j);
+      }
       mbar_wait(&pv_done[t], (nkv - 1) & 1);
       tc_fence_after();
-      l = final_l<HD, BKV, NQ>(o_tm, l);
-      if constexpr (SPEC) flag_overflow(l, overflow_flag);
-      store_o<HD>(o_tm, l, out + static_cast<int64_t>(s_begin + row) * d_model + head * HD, row < len);
+      if (h == 0) {
+        l = final_l<HD, BKV, NQ>(o_tm, l);
+        if constexpr (SPEC) flag_overflow(l, overflow_flag);
+        store_o<HD>(o_tm, l, out + static_cast<int64_t>(s_begin + row) * d_model + head * HD, row < len);
+      } else if constexpr (SPEC) {
+        flag_overflow(l, overflow_flag);  // the other half's wrap flag (its l is 0 or inf)
+      }
     }
   }
 
@@ -596,7 +718,7 @@ struct TcPersistLayout {
 // `gate`: when non-null the launch is the exact redo of a speculative pass and exits at once
 // unless that pass flagged an overflow.
 template <int HD, int BKV, int NQ, bool SPEC>
-__global__ void __maxnreg__(NQ == 2 ? 168 : 128)
+__global__ void __maxnreg__(MMK_ATTN_SPLIT && HD == 80 ? 96 : (NQ == 2 ? 168 : 128))
 attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_q_rem,
                        const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_kv_rem,
                        __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ cu_seqlens, int n_seq,
@@ -608,7 +730,8 @@ attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_co
   }
   using C = TcAttnCfg<HD, BKV, NQ>;
   using Lay = TcPersistLayout<HD, BKV, NQ>;
-  constexpr int kTmaWarp = 4 * NQ, kMmaWarp = 4 * NQ + 1;  // MMA warp of query tile t: kMmaWarp + t
+  constexpr int kTmaWarp = C::kSoftmaxWarps, kMmaWarp = C::kSoftmaxWarps + 1;  // MMA warp of tile t: kMmaWarp + t
+  __shared__ float s_red[C::kSplit ? 4 * NQ * 64 : 1];  // split softmax: row-max exchange
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::kBarOff);
@@ -653,14 +776,14 @@ attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_co
     }
     for (int t = 0; t < NQ; ++t) {
       mbar_init(&s_full[t], 1);
-      mbar_init(&s_free[t], 4);
-      mbar_init(&p_full[t], 4);
+      mbar_init(&s_free[t], 4 * C::kHalves);
+      mbar_init(&p_full[t], 4 * C::kHalves);
       mbar_init(&pv_done[t], 1);
       mbar_init(&o_free[t], 4);
     }
     for (int i = 0; i < 4; ++i) {
       mbar_init(&item_full[i], 1);
-      mbar_init(&item_empty[i], 5 * NQ);  // MMA warps + softmax warps
+      mbar_init(&item_empty[i], C::kSoftmaxWarps + NQ);  // MMA warps + softmax warps
     }
     fence_barrier_init();
   }
@@ -858,7 +981,8 @@ attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_co
     }
   } else {
     // ---------------------------------------------------------------- softmax warpgroups
-    const int t = warp >> 2;
+    const int t = warp / (4 * C::kHalves);
+    const int h = (warp >> 2) % C::kHalves;
     const uint32_t q4 = warp & 3;
     const uint32_t lane_base = (q4 * 32u) << 16;
     const uint32_t s_tm = tmem + t * BKV + lane_base;
@@ -870,19 +994,29 @@ attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_co
       if (it.len < 0) break;
       if (t >= it.n_qt) continue;  // also skips empty items (n_qt == 0)
       float m_used = -INFINITY, l = 0.f;
-      for (int j = 0; j < it.nkv; ++j)
-        softmax_tile<HD, BKV, NQ, SPEC>(s_tm, o_tm, p_tm, &s_full[t], &s_free[t], &pv_done[t], &p_full[t], g + j,
-                                        j == 0, it.len - j * BKV, scale_log2, m_used, l, lane, false, t, j);
+      for (int j = 0; j < it.nkv; ++j) {
+        if constexpr (C::kSplit)
+          softmax_tile_split<HD, BKV, NQ, SPEC>(s_tm, o_tm, p_tm, &s_full[t], &s_free[t], &pv_done[t], &p_full[t],
+                                                g + j, j == 0, it.len - j * BKV, scale_log2, m_used, l, lane, h,
+                                                s_red + (t * 4 + q4) * 64, 1 + t * 4 + q4);
+        else
+          softmax_tile<HD, BKV, NQ, SPEC>(s_tm, o_tm, p_tm, &s_full[t], &s_free[t], &pv_done[t], &p_full[t], g + j,
+                                          j == 0, it.len - j * BKV, scale_log2, m_used, l, lane, false, t, j);
+      }
       g += it.nkv;
       mbar_wait(&pv_done[t], (g - 1) & 1);
       tc_fence_after();
-      l = final_l<HD, BKV, NQ>(o_tm, l);
-      if constexpr (SPEC) flag_overflow(l, overflow_flag);
-      const int row = it.q0 + t * kTcBQ + q4 * 32 + lane;
-      store_o<HD>(o_tm, l, out + static_cast<int64_t>(it.s_begin + row) * d_model + it.head * HD, row < it.len);
-      tc_fence_before();  // O_t reads complete before the next item's first PV overwrites it
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&o_free[t]);
+      if (h == 0) {
+        l = final_l<HD, BKV, NQ>(o_tm, l);
+        if constexpr (SPEC) flag_overflow(l, overflow_flag);
+        const int row = it.q0 + t * kTcBQ + q4 * 32 + lane;
+        store_o<HD>(o_tm, l, out + static_cast<int64_t>(it.s_begin + row) * d_model + it.head * HD, row < it.len);
+        tc_fence_before();  // O_t reads complete before the next item's first PV overwrites it
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&o_free[t]);
+      } else if constexpr (SPEC) {
+        flag_overflow(l, overflow_flag);
+      }
     }
   }
 
