@@ -10,7 +10,7 @@
  *   core.tile_count / image_tokens      core.py:58-74              mmk_tile_plan   (K0, bit-exact)
  *   Request.total_image_tokens/tiles    core.py:110-120            mmk_tile_plan   (int64 offsets)
  *   LatencyProfile.preprocess_latency   profiles.py:128-134        mmk_preprocess  (K1)
- *   LatencyProfile.encode_latency       profiles.py:136-145        mmk_gemm_bf16 / mmk_layernorm_f32
+ *   LatencyProfile.encode_latency       profiles.py:136-145        mmk_gemm_bf16(_ln) / mmk_layernorm
  *                                                                  / mmk_attention_varlen_bf16 /
  *                                                                  mmk_embed_* (K2-K8)
  *   shard join + handoff                engine.py:730-752, :563-579 mmk_pack_mllama_peer (K9+K10 fused:
@@ -60,7 +60,8 @@ const char* mmk_last_error(void);
  *        ar_id[n] (optional) = 1 + index of (rows, cols) in the enumeration of all (a, b) with
  *        a*b <= cap, a outer (transformers Mllama supported_aspect_ratios; 0 = no image);
  *        bad[1] (int32) = number of images with w<1 or h<1 (their tiles are 0).
- * Single launch, one CTA, n <= 65536.
+ * Two launches: a thread per image (count, canvas, aspect-ratio id), then one CTA scanning the
+ * counts into the int64 offsets; n <= 65536.
  */
 int mmk_tile_plan(const int32_t* w, const int32_t* h, int32_t n, int32_t tile_px,
                   int32_t tokens_per_tile, int32_t max_tiles, int32_t thumbnail,
@@ -104,6 +105,23 @@ int mmk_preprocess(const uint8_t* src, const int64_t* src_off, int32_t src_chw, 
 int mmk_gemm_bf16(const void* a, int64_t lda, const void* b, int64_t ldb, int32_t m, int32_t n,
                   int32_t k, int32_t epilogue, const float* bias, void* out, int64_t ldo,
                   float gate, void* aux, int64_t ld_aux, cudaStream_t stream);
+
+/*
+ * The same GEMM with a LayerNorm folded into the residual GEMM before it and the GEMM after it
+ * (no separate LayerNorm pass over the residual stream):
+ *   producer  (RESID_F32): ln_stats_out f32 [m][n/32][2] = (mean, M2) of each 32-column chunk of
+ *             the updated residual row; `aux` receives the bf16 copy of the row.
+ *   finalize  mmk_ln_stats_finalize: stats -> ln_mr f32 [m][2] = (mean, 1/sqrt(var + eps)).
+ *   consumer  (bf16 epilogues): a = that bf16 copy, b = W * gamma (gamma along K), ln_c1 f32 [n] =
+ *             row sums of b, bias = beta . W^T + b:  out = act(rstd * (acc - mean * c1) + bias).
+ * Pointers 16-byte aligned; NULL where unused.
+ */
+int mmk_gemm_bf16_ln(const void* a, int64_t lda, const void* b, int64_t ldb, int32_t m, int32_t n,
+                     int32_t k, int32_t epilogue, const float* bias, void* out, int64_t ldo,
+                     float gate, void* aux, int64_t ld_aux, float* ln_stats_out, const float* ln_mr,
+                     const float* ln_c1, cudaStream_t stream);
+int mmk_ln_stats_finalize(const float* stats, int32_t rows, int32_t d, float eps, float* mr,
+                          cudaStream_t stream);
 
 /*
  * K3 — row LayerNorm: y_bf16 = LN(x_f32) * gamma + beta (+ optional per-tile additive term).

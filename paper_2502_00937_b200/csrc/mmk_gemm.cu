@@ -97,14 +97,52 @@ MMK_DEV float apply_act(float v) {
   else return v;
 }
 
+// LayerNorm folded into the GEMMs around it (the LN between a residual update and the GEMM that
+// consumes the normalised rows):
+//   producer (RESID_F32): besides the fp32 residual, the bf16 copy of the new row goes to `aux`
+//     and each 32-column chunk's (mean, M2) to stats_out[row][col / 32] (exact two-pass inside
+//     the chunk; mmk_ln_stats_finalize merges the chunks, Chan's formula, into (mu, rstd)).
+//   consumer (bf16 epilogues): A = that bf16 copy, B = W (x) gamma; out = act(rstd * (acc - mu *
+//     c1[n]) + bias[n]) with c1[n] = sum_k W'[n,k] and bias = beta W^T + b (host-prepared).
+struct LnFold {
+  float2* stats_out;   // producer: [M][N/32] (mean, M2) per 32-column chunk, or null
+  const float2* mr;    // consumer: [M] (mu, rstd), or null
+  const float* c1;     // consumer: [N]
+};
+
+MMK_DEV void chunk_stats(const float (&v)[32], float2* dst) {
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) s += v[i];
+  const float mean = s * (1.f / 32.f);
+  float m2 = 0.f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const float d = v[i] - mean;
+    m2 = fmaf(d, d, m2);
+  }
+  *dst = make_float2(mean, m2);
+}
+
 // Fused epilogue for 32 consecutive accumulator columns of one output row (thread-owned row).
 template <int EPI>
 MMK_DEV void epilogue_chunk(const uint32_t (&r)[32], int row, int col, const float* __restrict__ bias, void* out,
-                            int64_t ldo, float gate, __nv_bfloat16* __restrict__ aux, int64_t ld_aux) {
+                            int64_t ldo, float gate, __nv_bfloat16* __restrict__ aux, int64_t ld_aux,
+                            const LnFold& lf, float2 mr, int n_total) {
   float v[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-  if (bias != nullptr) {
+  if (lf.c1 != nullptr) {  // folded LayerNorm: rstd * (acc - mu * c1) + bias
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      const float4 c4 = __ldg(reinterpret_cast<const float4*>(lf.c1 + col + i));
+      const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + col + i));
+      v[i] = fmaf(mr.y, fmaf(-mr.x, c4.x, v[i]), b4.x);
+      v[i + 1] = fmaf(mr.y, fmaf(-mr.x, c4.y, v[i + 1]), b4.y);
+      v[i + 2] = fmaf(mr.y, fmaf(-mr.x, c4.z, v[i + 2]), b4.z);
+      v[i + 3] = fmaf(mr.y, fmaf(-mr.x, c4.w, v[i + 3]), b4.w);
+    }
+  } else if (bias != nullptr) {
 #pragma unroll
     for (int i = 0; i < 32; i += 4) {
       const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + col + i));
@@ -135,6 +173,7 @@ MMK_DEV void epilogue_chunk(const uint32_t (&r)[32], int row, int col, const flo
         st_global_v4(ao + i, pack_bf16x2(v[i], v[i + 1]), pack_bf16x2(v[i + 2], v[i + 3]),
                      pack_bf16x2(v[i + 4], v[i + 5]), pack_bf16x2(v[i + 6], v[i + 7]));
     }
+    if (lf.stats_out != nullptr) chunk_stats(v, lf.stats_out + static_cast<int64_t>(row) * (n_total / 32) + col / 32);
   } else {
     __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + static_cast<int64_t>(row) * ldo + col;
 #pragma unroll
@@ -150,7 +189,7 @@ template <int BN, int STAGES, int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                   int M, int N, int K, const float* __restrict__ bias, void* __restrict__ out,
-                  int64_t ldo, float gate, __nv_bfloat16* __restrict__ aux, int64_t ld_aux) {
+                  int64_t ldo, float gate, __nv_bfloat16* __restrict__ aux, int64_t ld_aux, LnFold lf) {
   using S = GemmSmem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -258,6 +297,7 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
       const bool row_ok = row < M;
+      const float2 mr = lf.mr != nullptr ? lf.mr[row_ok ? row : M - 1] : make_float2(0.f, 1.f);
 #pragma unroll 1
       for (int c = 0; c < kColsPerWarp / 32; ++c) {
         const int col_in_tile = half * kColsPerWarp + c * 32;
@@ -266,7 +306,7 @@ gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap tmap_a, const __grid_const
         tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + acc * BN + col_in_tile, r);
         tmem_ld_wait();
         if (!row_ok || col >= N) continue;
-        epilogue_chunk<EPI>(r, row, col, bias, out, ldo, gate, aux, ld_aux);
+        epilogue_chunk<EPI>(r, row, col, bias, out, ldo, gate, aux, ld_aux, lf, mr, N);
       }
       tc_fence_before();
       __syncwarp();
@@ -307,7 +347,8 @@ struct Gemm2Smem {
 // tensor store; two buffers per warp so the store of one chunk overlaps the next chunk.
 template <int EPI>
 MMK_DEV void epilogue_bf16_tma(const uint32_t (&r0)[32], const uint32_t (&r1)[32], int col, int row0, uint32_t lane,
-                               const float* __restrict__ bias, uint8_t* buf, const CUtensorMap* tmap_out) {
+                               const float* __restrict__ bias, uint8_t* buf, const CUtensorMap* tmap_out,
+                               const float* __restrict__ c1 = nullptr, float2 mr = make_float2(0.f, 1.f)) {
   uint32_t w[32];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -316,7 +357,13 @@ MMK_DEV void epilogue_bf16_tma(const uint32_t (&r0)[32], const uint32_t (&r1)[32
     for (int i = 0; i < 32; i += 4) {
       float2 a = make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1]));
       float2 b = make_float2(__uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
-      if (bias != nullptr) {  // one 16-byte broadcast load per 4 columns
+      if (c1 != nullptr) {  // folded LayerNorm: rstd * (acc - mu * c1) + bias
+        const float4 c4 = __ldg(reinterpret_cast<const float4*>(c1 + col + 32 * h + i));
+        const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + col + 32 * h + i));
+        const float2 nmu = make_float2(-mr.x, -mr.x), rs = make_float2(mr.y, mr.y);
+        a = __ffma2_rn(rs, __ffma2_rn(nmu, make_float2(c4.x, c4.y), a), make_float2(b4.x, b4.y));
+        b = __ffma2_rn(rs, __ffma2_rn(nmu, make_float2(c4.z, c4.w), b), make_float2(b4.z, b4.w));
+      } else if (bias != nullptr) {  // one 16-byte broadcast load per 4 columns
         const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + col + 32 * h + i));
         a = __fadd2_rn(a, make_float2(b4.x, b4.y));
         b = __fadd2_rn(b, make_float2(b4.z, b4.w));
@@ -348,7 +395,7 @@ template <int STAGES, int EPI, bool RES_TMA = false>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                       const __grid_constant__ CUtensorMap tmap_out, int M, int N, int K, const float* __restrict__ bias, void* __restrict__ out, int64_t ldo,
-                      float gate, __nv_bfloat16* __restrict__ aux, int64_t ld_aux) {
+                      float gate, __nv_bfloat16* __restrict__ aux, int64_t ld_aux, LnFold lf) {
   using S = Gemm2Smem<STAGES>;
   constexpr int BN = kGemm2BN;
   extern __shared__ uint8_t smem_raw[];
@@ -485,6 +532,8 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
       tc_fence_after();
       const uint32_t tm_row = tmem_base + ((q * 32u) << 16) + acc * BN;
       if constexpr (kTmaStore) {
+        const int mrow = m0 + static_cast<int>(q) * 32 + static_cast<int>(lane);
+        const float2 mr = lf.mr != nullptr ? lf.mr[mrow < M ? mrow : M - 1] : make_float2(0.f, 1.f);
 #pragma unroll 1
         for (int c = 0; c < kColsPerWarp / 64; ++c) {
           const int col_in_tile = half * kColsPerWarp + c * 64;
@@ -498,7 +547,7 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
             if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
           }
           epilogue_bf16_tma<EPI>(r0, r1, n0 + col_in_tile, m0 + static_cast<int>(q) * 32, lane, bias,
-                                 ebuf + sb * 4096, &tmap_out);
+                                 ebuf + sb * 4096, &tmap_out, lf.c1, mr);
           sb ^= 1;
         }
       } else if constexpr (RES_TMA) {
@@ -544,15 +593,28 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
             *p4 = rr;
             v[4 * j] = rr.x; v[4 * j + 1] = rr.y; v[4 * j + 2] = rr.z; v[4 * j + 3] = rr.w;
           }
-          if (aux != nullptr && row_ok) {
-            __nv_bfloat16* ao = aux + static_cast<int64_t>(row) * ld_aux + col;
-#pragma unroll
-            for (int i = 0; i < 32; i += 8)
-              st_global_v4(ao + i, pack_bf16x2(v[i], v[i + 1]), pack_bf16x2(v[i + 2], v[i + 3]),
-                           pack_bf16x2(v[i + 4], v[i + 5]), pack_bf16x2(v[i + 6], v[i + 7]));
-          }
+          if (lf.stats_out != nullptr && row_ok)
+            chunk_stats(v, lf.stats_out + static_cast<int64_t>(row) * (N / 32) + col / 32);
           fence_proxy_async();
           __syncwarp();
+          if (aux != nullptr) {
+            // bf16 copy of the updated 32x32 chunk, read back from the slot transposed so that a
+            // warp store covers 8 whole 64-byte row segments (a row per lane would scatter each
+            // store over 32 rows): lane = 4 r + cc writes columns 8cc..8cc+7 of row 8k + r
+            const int rr0 = static_cast<int>(lane >> 2), cc = static_cast<int>(lane & 3);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const int rr = 8 * kk + rr0;
+              const uint8_t* src = ebuf + slot * 4096 + rr * 128;
+              const float4 lo = *reinterpret_cast<const float4*>(src + (((2 * cc) ^ (rr & 7)) << 4));
+              const float4 hi = *reinterpret_cast<const float4*>(src + (((2 * cc + 1) ^ (rr & 7)) << 4));
+              const int grow = m0 + static_cast<int>(q) * 32 + rr;
+              if (grow < M)
+                st_global_v4(aux + static_cast<int64_t>(grow) * ld_aux + col + 8 * cc, pack_bf16x2(lo.x, lo.y),
+                             pack_bf16x2(lo.z, lo.w), pack_bf16x2(hi.x, hi.y), pack_bf16x2(hi.z, hi.w));
+            }
+            __syncwarp();  // the slot may be refilled after this
+          }
           if (lane == 0) {
             tma_store_2d(&tmap_out, ebuf + slot * 4096, col, m0 + static_cast<int>(q) * 32);
             tma_store_commit();
@@ -618,7 +680,8 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
           tmem_ld_32x32b_x32(tm_row + col_in_tile, r);
           tmem_ld_wait();
           if (!row_ok) continue;
-          epilogue_chunk<EPI>(r, row, col, bias, out, ldo, gate, aux, ld_aux);
+          epilogue_chunk<EPI>(r, row, col, bias, out, ldo, gate, aux, ld_aux, lf,
+                              lf.mr != nullptr ? lf.mr[row] : make_float2(0.f, 1.f), N);
         }
         tc_fence_before();
         __syncwarp();
@@ -641,7 +704,7 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
 template <int BN, int STAGES, int EPI>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
                        const float* bias, void* out, int64_t ldo, float gate, __nv_bfloat16* aux,
-                       int64_t ld_aux, cudaStream_t stream) {
+                       int64_t ld_aux, const LnFold& lf, cudaStream_t stream) {
   using S = GemmSmem<BN, STAGES>;
   auto kern = gemm_bf16_tcgen05<BN, STAGES, EPI>;
   static std::atomic<uint64_t> attr_done{0};  // per template instance
@@ -650,7 +713,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int 
   const int tiles = ((M + kGemmBM - 1) / kGemmBM) * ((N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   cudaError_t e = launch_kernel(kern, dim3(grid), dim3(kGemmThreads), S::kTotal, stream, 1, tiles <= 2 * num_sms(), ta, tb, M, N, K, bias,
-                                out, ldo, gate, aux, ld_aux);
+                                out, ldo, gate, aux, ld_aux, lf);
   if (e != cudaSuccess) return set_cuda_error(e, "gemm: launch");
   return MMK_OK;
 }
@@ -658,13 +721,13 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, int M, int 
 template <int BN, int STAGES>
 static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
                         const float* bias, void* out, int64_t ldo, float gate, __nv_bfloat16* aux,
-                        int64_t ld_aux, cudaStream_t s) {
+                        int64_t ld_aux, const LnFold& lf, cudaStream_t s) {
   switch (epi) {
-    case MMK_EPI_BF16: return launch_gemm<BN, STAGES, MMK_EPI_BF16>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
-    case MMK_EPI_BF16_GELU: return launch_gemm<BN, STAGES, MMK_EPI_BF16_GELU>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
-    case MMK_EPI_BF16_QUICKGELU: return launch_gemm<BN, STAGES, MMK_EPI_BF16_QUICKGELU>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
-    case MMK_EPI_F32: return launch_gemm<BN, STAGES, MMK_EPI_F32>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
-    case MMK_EPI_RESID_F32: return launch_gemm<BN, STAGES, MMK_EPI_RESID_F32>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
+    case MMK_EPI_BF16: return launch_gemm<BN, STAGES, MMK_EPI_BF16>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
+    case MMK_EPI_BF16_GELU: return launch_gemm<BN, STAGES, MMK_EPI_BF16_GELU>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
+    case MMK_EPI_BF16_QUICKGELU: return launch_gemm<BN, STAGES, MMK_EPI_BF16_QUICKGELU>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
+    case MMK_EPI_F32: return launch_gemm<BN, STAGES, MMK_EPI_F32>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
+    case MMK_EPI_RESID_F32: return launch_gemm<BN, STAGES, MMK_EPI_RESID_F32>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
     default: return set_error(MMK_ERR_ARG, "gemm: unknown epilogue %d", epi);
   }
 }
@@ -674,7 +737,7 @@ template <int STAGES, int EPI, bool RES_TMA = false>
 static int launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, int M, int N, int K,
                            const float* bias,
                            void* out, int64_t ldo, float gate, __nv_bfloat16* aux, int64_t ld_aux,
-                           cudaStream_t stream) {
+                           const LnFold& lf, cudaStream_t stream) {
   using S = Gemm2Smem<STAGES>;
   auto kern = gemm_bf16_tcgen05_2sm<STAGES, EPI, RES_TMA>;
   static std::atomic<uint64_t> attr_done{0};  // per template instance
@@ -684,7 +747,7 @@ static int launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, const C
   const int pairs_max = num_sms() / 2;
   const int pairs = tiles < pairs_max ? tiles : pairs_max;
   cudaError_t e = launch_kernel(kern, dim3(2 * pairs), dim3(kGemmThreads), S::kTotal, stream, 2, tiles <= num_sms(), ta, tb, to, M, N, K,
-                                bias, out, ldo, gate, aux, ld_aux);
+                                bias, out, ldo, gate, aux, ld_aux, lf);
   if (e != cudaSuccess) return set_cuda_error(e, "gemm2: launch");
   return MMK_OK;
 }
@@ -692,16 +755,16 @@ static int launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, const C
 template <int STAGES>
 static int dispatch_epi_2sm(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, int M,
                             int N, int K, const float* bias, void* out, int64_t ldo, float gate,
-                            __nv_bfloat16* aux, int64_t ld_aux, cudaStream_t s) {
+                            __nv_bfloat16* aux, int64_t ld_aux, const LnFold& lf, cudaStream_t s) {
   switch (epi) {
-    case MMK_EPI_BF16: return launch_gemm_2sm<STAGES, MMK_EPI_BF16>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
-    case MMK_EPI_BF16_GELU: return launch_gemm_2sm<STAGES, MMK_EPI_BF16_GELU>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
-    case MMK_EPI_BF16_QUICKGELU: return launch_gemm_2sm<STAGES, MMK_EPI_BF16_QUICKGELU>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
-    case MMK_EPI_F32: return launch_gemm_2sm<STAGES, MMK_EPI_F32>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
+    case MMK_EPI_BF16: return launch_gemm_2sm<STAGES, MMK_EPI_BF16>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
+    case MMK_EPI_BF16_GELU: return launch_gemm_2sm<STAGES, MMK_EPI_BF16_GELU>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
+    case MMK_EPI_BF16_QUICKGELU: return launch_gemm_2sm<STAGES, MMK_EPI_BF16_QUICKGELU>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
+    case MMK_EPI_F32: return launch_gemm_2sm<STAGES, MMK_EPI_F32>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
     case MMK_EPI_RESID_F32:
       // the fp32 residual streams through shared memory by TMA (O-proj 0.420 -> 0.365 ms, FC2
       // 1.165 -> 1.137 ms versus a direct read-modify-write from the epilogue registers)
-      return launch_gemm_2sm<STAGES, MMK_EPI_RESID_F32, true>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, s);
+      return launch_gemm_2sm<STAGES, MMK_EPI_RESID_F32, true>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
     default: return set_error(MMK_ERR_ARG, "gemm: unknown epilogue %d", epi);
   }
 }
@@ -709,9 +772,10 @@ static int dispatch_epi_2sm(int epi, const CUtensorMap& ta, const CUtensorMap& t
 
 using namespace mmk;
 
-extern "C" int mmk_gemm_bf16(const void* a, int64_t lda, const void* b, int64_t ldb, int32_t m,
-                             int32_t n, int32_t k, int32_t epilogue, const float* bias, void* out,
-                             int64_t ldo, float gate, void* aux, int64_t ld_aux, cudaStream_t stream) {
+extern "C" int mmk_gemm_bf16_ln(const void* a, int64_t lda, const void* b, int64_t ldb, int32_t m,
+                                int32_t n, int32_t k, int32_t epilogue, const float* bias, void* out,
+                                int64_t ldo, float gate, void* aux, int64_t ld_aux, float* ln_stats_out,
+                                const float* ln_mr, const float* ln_c1, cudaStream_t stream) {
   if (m < 0 || n <= 0 || k <= 0) return set_error(MMK_ERR_ARG, "gemm: bad shape m=%d n=%d k=%d", m, n, k);
   if (m == 0) return MMK_OK;
   if (n % 32 != 0) return set_error(MMK_ERR_UNSUPPORTED, "gemm: N=%d must be a multiple of 32", n);
@@ -724,6 +788,15 @@ extern "C" int mmk_gemm_bf16(const void* a, int64_t lda, const void* b, int64_t 
   if (ldo % (f32_out ? 4 : 8) != 0) return set_error(MMK_ERR_ARG, "gemm: ldo misaligned");
   if (aux != nullptr && (epilogue != MMK_EPI_RESID_F32 || ld_aux % 8 != 0))
     return set_error(MMK_ERR_ARG, "gemm: aux output only with RESID_F32 and 16B-aligned rows");
+  if (ln_stats_out != nullptr && epilogue != MMK_EPI_RESID_F32)
+    return set_error(MMK_ERR_ARG, "gemm: LN statistics only from a RESID_F32 epilogue");
+  if ((ln_mr != nullptr) != (ln_c1 != nullptr) ||
+      (ln_mr != nullptr && (epilogue == MMK_EPI_F32 || epilogue == MMK_EPI_RESID_F32 || bias == nullptr)))
+    return set_error(MMK_ERR_ARG, "gemm: a folded LayerNorm needs mr, c1 and bias with a bf16 epilogue");
+  if ((reinterpret_cast<uintptr_t>(ln_c1) | reinterpret_cast<uintptr_t>(ln_mr) |
+       reinterpret_cast<uintptr_t>(ln_stats_out)) & 15)
+    return set_error(MMK_ERR_ARG, "gemm: LN pointers must be 16-byte aligned");
+  const LnFold lf{reinterpret_cast<float2*>(ln_stats_out), reinterpret_cast<const float2*>(ln_mr), ln_c1};
   // Kernel choice: CTA pairs (M=256 x N=256 tiles) when N splits into 256-wide tiles and there
   // are enough tiles to occupy the pairs; otherwise the single-CTA kernel with BN 256 or 128.
   static const bool no_2sm = getenv("MMK_GEMM_NO_2SM") != nullptr;  // A/B switch for profiling
@@ -746,7 +819,7 @@ extern "C" int mmk_gemm_bf16(const void* a, int64_t lda, const void* b, int64_t 
       if (rc) return rc;
     }
     return dispatch_epi_2sm<5>(epilogue, ta, tb, to, m, n, k, bias, out, ldo, gate,
-                               reinterpret_cast<__nv_bfloat16*>(aux), ld_aux, stream);
+                               reinterpret_cast<__nv_bfloat16*>(aux), ld_aux, lf, stream);
   }
   const int tiles256 = ((m + kGemmBM - 1) / kGemmBM) * ((n + 255) / 256);
   const bool use128 = (n % 256 != 0) || tiles256 < num_sms();
@@ -757,7 +830,14 @@ extern "C" int mmk_gemm_bf16(const void* a, int64_t lda, const void* b, int64_t 
   if (rc) return rc;
   if (use128)
     return dispatch_epi<128, 6>(epilogue, ta, tb, m, n, k, bias, out, ldo, gate,
-                                reinterpret_cast<__nv_bfloat16*>(aux), ld_aux, stream);
+                                reinterpret_cast<__nv_bfloat16*>(aux), ld_aux, lf, stream);
   return dispatch_epi<256, 4>(epilogue, ta, tb, m, n, k, bias, out, ldo, gate,
-                              reinterpret_cast<__nv_bfloat16*>(aux), ld_aux, stream);
+                              reinterpret_cast<__nv_bfloat16*>(aux), ld_aux, lf, stream);
+}
+
+extern "C" int mmk_gemm_bf16(const void* a, int64_t lda, const void* b, int64_t ldb, int32_t m,
+                             int32_t n, int32_t k, int32_t epilogue, const float* bias, void* out,
+                             int64_t ldo, float gate, void* aux, int64_t ld_aux, cudaStream_t stream) {
+  return mmk_gemm_bf16_ln(a, lda, b, ldb, m, n, k, epilogue, bias, out, ldo, gate, aux, ld_aux, nullptr, nullptr,
+                          nullptr, stream);
 }

@@ -292,6 +292,28 @@ __global__ void checksum_kernel(const __nv_bfloat16* __restrict__ x, int64_t n, 
 
 static int grid_rows(int64_t rows) { return static_cast<int>((rows + 7) / 8); }
 
+// Folded LayerNorm: the producer GEMM's per-32-column (mean, M2) of a row -> (mu, rstd), merged
+// with Chan's formula (equal chunk counts); a thread per row.
+__global__ void ln_stats_finalize_kernel(const float2* __restrict__ stats, int rows, int parts, float inv_d, float eps,
+                                         float2* __restrict__ mr) {
+  griddep_wait();  // PDL: the statistics come from the preceding GEMM
+  griddep_launch_dependents();
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  const float2* s = stats + static_cast<int64_t>(row) * parts;
+  float2 a = s[0];
+  float n = 32.f;
+  for (int i = 1; i < parts; ++i) {
+    const float2 b = s[i];
+    const float nn = n + 32.f;
+    const float delta = b.x - a.x;
+    a.x = fmaf(delta, 32.f / nn, a.x);
+    a.y = a.y + b.y + delta * delta * (n * 32.f / nn);
+    n = nn;
+  }
+  mr[row] = make_float2(a.x, rsqrtf(fmaf(a.y, inv_d, eps)));
+}
+
 }  // namespace mmk
 
 using namespace mmk;
@@ -427,4 +449,15 @@ extern "C" int mmk_checksum_bf16(const void* x, int64_t n, float* out, cudaStrea
   (void)launch_kernel(checksum_kernel, dim3(4 * num_sms()), dim3(256), 0, stream, 1, n <= 1024 * kSmallRows, reinterpret_cast<const __nv_bfloat16*>(x), n, out);
   e = cudaGetLastError();
   return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "checksum: launch");
+}
+
+extern "C" int mmk_ln_stats_finalize(const float* stats, int32_t rows, int32_t d, float eps, float* mr,
+                                     cudaStream_t stream) {
+  if (rows < 0 || d < 32 || d % 32 != 0) return set_error(MMK_ERR_ARG, "ln_stats_finalize: rows < 0 or d %% 32 != 0");
+  if (rows == 0) return MMK_OK;
+  (void)launch_kernel(ln_stats_finalize_kernel, dim3((rows + 255) / 256), dim3(256), 0, stream, 1, rows <= kSmallRows,
+                      reinterpret_cast<const float2*>(stats), rows, d / 32, 1.f / static_cast<float>(d), eps,
+                      reinterpret_cast<float2*>(mr));
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "ln_stats_finalize: launch");
 }

@@ -20,6 +20,7 @@ Weights are random-initialised from a seed (no checkpoints in this environment).
 from __future__ import annotations
 
 import math
+import os
 
 import torch
 
@@ -32,7 +33,7 @@ from .weights import K_ALIGN, init_weights, k_pad_of  # noqa: F401  (re-exported
 class DeviceEncoder:
     """Device-resident weights + the forward of one encoder over a ragged batch of tiles."""
 
-    def __init__(self, spec: ModelSpec, weights: dict, device="cuda"):
+    def __init__(self, spec: ModelSpec, weights: dict, device="cuda", fold_ln: bool | None = None):
         enc = spec.encoder
         if enc is None:
             raise SpecError(f"{spec.name}: no encoder block")
@@ -40,6 +41,9 @@ class DeviceEncoder:
             from ._lib import ProfileError
             raise ProfileError(f"{spec.name}: head_dim {enc.head_dim} not supported by the attention kernel")
         self.spec, self.enc, self.device = spec, enc, torch.device(device)
+        # LayerNorm folded into the GEMMs (mmk_gemm_bf16_ln): every LN whose input comes from a
+        # residual GEMM; MMK_LN_FOLD=0 runs the separate LayerNorm kernel instead (A/B runs)
+        self.fold_ln = (os.environ.get("MMK_LN_FOLD", "1") != "0") if fold_ln is None else fold_ln
         self.P = (spec.tile_edge_px // enc.patch_px) ** 2
         self.k_pad = k_pad_of(spec)
         dev = self.device
@@ -53,8 +57,16 @@ class DeviceEncoder:
         self.pre_ln = (f32(weights["pre_ln_w"]), f32(weights["pre_ln_b"]))
         self.post_ln = (f32(weights["post_ln_w"]), f32(weights["post_ln_b"]))
 
+        def folded(w, g, b, bias):
+            """(W * gamma in bf16, c1 = row sums of it, c2 = beta W^T + bias): a LayerNorm with
+            (gamma, beta) in front of the GEMM W folded into the GEMM (see mmk_gemm_bf16_ln)."""
+            wf = (w.double() * g.double()[None, :]).to(torch.bfloat16)
+            c1 = wf.double().sum(1)
+            c2 = w.double() @ b.double() + (bias.double() if bias is not None else 0.0)
+            return bf(wf), f32(c1.float()), f32(c2.float())
+
         def block(pre, gated):
-            return {
+            L = {
                 "ln1": (f32(weights[pre + "ln1_w"]), f32(weights[pre + "ln1_b"])),
                 "qkv_w": bf(weights[pre + "qkv_w"]), "qkv_b": f32(weights.get(pre + "qkv_b")),
                 "o_w": bf(weights[pre + "o_w"]), "o_b": f32(weights.get(pre + "o_b")),
@@ -64,6 +76,12 @@ class DeviceEncoder:
                 "gate_attn": math.tanh(float(weights[pre + "gate_attn"])) if gated else 1.0,
                 "gate_ffn": math.tanh(float(weights[pre + "gate_ffn"])) if gated else 1.0,
             }
+            if self.fold_ln:
+                L["qkv_f"] = folded(weights[pre + "qkv_w"], weights[pre + "ln1_w"], weights[pre + "ln1_b"],
+                                    weights.get(pre + "qkv_b"))
+                L["fc1_f"] = folded(weights[pre + "fc1_w"], weights[pre + "ln2_w"], weights[pre + "ln2_b"],
+                                    weights[pre + "fc1_b"])
+            return L
 
         self.layers = [block(f"l{i}.", False) for i in range(enc.layers)]
         self.global_layers = [block(f"g{i}.", True) for i in range(enc.global_layers)]
@@ -82,15 +100,56 @@ class DeviceEncoder:
         self.norm_shift = (-mean / std).to(torch.float32).to(dev)
 
     # ------------------------------------------------------------------ layers
-    def _block(self, L, resid, x_buf, qkv_buf, h_buf, cu, n_seq, max_s, aux=None, sum_sq=0.0):
+    def _block(self, L, resid, x_buf, qkv_buf, h_buf, cu, n_seq, max_s, aux=None, sum_sq=0.0, ln=None, xr=None,
+               stats_next=False):
+        """One pre-LN block.  Folded LayerNorms (self.fold_ln): ``ln`` = (stats, mr) buffers; LN1
+        is folded when ``xr`` (the bf16 copy of the residual the previous FC2 wrote) is given, LN2
+        always; with ``stats_next`` the FC2 also emits the next block's LN statistics.  Returns the
+        bf16 copy of the updated residual (for the next block's folded LN1) or None."""
         enc = self.enc
-        ops.layernorm(resid, *L["ln1"], enc.norm_eps, out=x_buf)
-        ops.gemm(x_buf, L["qkv_w"], ops.EPI_BF16, bias=L["qkv_b"], out=qkv_buf)
+        T, d = resid.shape
+        if xr is not None:  # LN1 folded: QKV = act-free epilogue rstd * (acc - mu c1) + c2
+            wf, c1, c2 = L["qkv_f"]
+            ops.gemm(xr, wf, ops.EPI_BF16, bias=c2, out=qkv_buf, ln_mr=ln[1], ln_c1=c1)
+        else:
+            ops.layernorm(resid, *L["ln1"], enc.norm_eps, out=x_buf)
+            ops.gemm(x_buf, L["qkv_w"], ops.EPI_BF16, bias=L["qkv_b"], out=qkv_buf)
         ops.attention(qkv_buf, cu, n_seq, max_s, enc.heads, enc.head_dim, out=x_buf, sum_sq_seqlen=sum_sq)
-        ops.gemm(x_buf, L["o_w"], ops.EPI_RESID_F32, bias=L["o_b"], out=resid, gate=L["gate_attn"])
-        ops.layernorm(resid, *L["ln2"], enc.norm_eps, out=x_buf)
-        ops.gemm(x_buf, L["fc1_w"], ops.ACT_EPI[enc.act], bias=L["fc1_b"], out=h_buf)
+        if ln is not None:
+            # the O-proj writes the residual's bf16 copy into the (now free) Q columns of qkv_buf
+            # and its LN statistics; FC1 consumes the copy with LN2 folded in
+            xr2 = qkv_buf[:, :d]
+            ops.gemm(x_buf, L["o_w"], ops.EPI_RESID_F32, bias=L["o_b"], out=resid, gate=L["gate_attn"], aux=xr2,
+                     ln_stats_out=ln[0])
+            ops.ln_stats_finalize(ln[0], T, d, enc.norm_eps, out=ln[1])
+            wf, c1, c2 = L["fc1_f"]
+            ops.gemm(xr2, wf, ops.ACT_EPI[enc.act], bias=c2, out=h_buf, ln_mr=ln[1], ln_c1=c1)
+        else:
+            ops.gemm(x_buf, L["o_w"], ops.EPI_RESID_F32, bias=L["o_b"], out=resid, gate=L["gate_attn"])
+            ops.layernorm(resid, *L["ln2"], enc.norm_eps, out=x_buf)
+            ops.gemm(x_buf, L["fc1_w"], ops.ACT_EPI[enc.act], bias=L["fc1_b"], out=h_buf)
+        if ln is not None and stats_next:
+            # the bf16 copy goes to the capture buffer when this layer is captured, else to x_buf
+            # (free: the attention output was consumed by the O-proj)
+            dst = aux if aux is not None else x_buf
+            ops.gemm(h_buf, L["fc2_w"], ops.EPI_RESID_F32, bias=L["fc2_b"], out=resid, gate=L["gate_ffn"], aux=dst,
+                     ln_stats_out=ln[0])
+            ops.ln_stats_finalize(ln[0], T, d, enc.norm_eps, out=ln[1])
+            return dst
         ops.gemm(h_buf, L["fc2_w"], ops.EPI_RESID_F32, bias=L["fc2_b"], out=resid, gate=L["gate_ffn"], aux=aux)
+        return None
+
+    def _run_layers(self, layers, resid, x_buf, qkv_buf, h_buf, cu, n_seq, max_s, sum_sq, aux_of=lambda i: None):
+        """A stack of blocks; with fold_ln only the stack's first LN1 runs as a LayerNorm kernel."""
+        T, d = resid.shape
+        ln = None
+        if self.fold_ln and d % 32 == 0:
+            ln = (torch.empty(T, d // 32, 2, dtype=torch.float32, device=resid.device),
+                  torch.empty(T, 2, dtype=torch.float32, device=resid.device))
+        xr = None
+        for i, L in enumerate(layers):
+            xr = self._block(L, resid, x_buf, qkv_buf, h_buf, cu, n_seq, max_s, aux=aux_of(i), sum_sq=sum_sq, ln=ln,
+                             xr=xr, stats_next=i + 1 < len(layers))
 
     def forward(self, patches: torch.Tensor, total_tiles: int, cu_seqlens: torch.Tensor, n_seq: int, max_seqlen: int,
                 tile_image=None, tile_slot=None, image_ar=None, out_alloc=None, sum_sq_seqlen: float = 0.0) -> torch.Tensor:
@@ -115,8 +174,8 @@ class DeviceEncoder:
         h_buf = torch.empty(T, enc.ffn, dtype=torch.bfloat16, device=dev)
         if enc.family == "clip":
             n_run = enc.layers if enc.out_layer == -1 else enc.layers + 1 + enc.out_layer
-            for L in self.layers[:n_run]:
-                self._block(L, resid, x_buf, qkv_buf, h_buf, cu_seqlens, n_seq, max_seqlen, sum_sq=sum_sq_seqlen)
+            self._run_layers(self.layers[:n_run], resid, x_buf, qkv_buf, h_buf, cu_seqlens, n_seq, max_seqlen,
+                             sum_sq_seqlen)
             # emitted = hidden_states[out_layer] as transformers' CLIPVisionModel numbers them
             # (modeling_clip.py: post_layernorm touches only the pooled CLS, never the sequence)
             drop = 1 if enc.drop_cls else 0
@@ -128,16 +187,18 @@ class DeviceEncoder:
         # transformers-5 "output of layer i")
         outs = list(enc.out_layers)
         inter = torch.empty(len(outs), T, d, dtype=torch.bfloat16, device=dev)
-        for i, L in enumerate(self.layers):
+
+        def aux_of(i):
             k = enc.capture_after(i)
-            aux = inter[k] if k is not None else None
-            self._block(L, resid, x_buf, qkv_buf, h_buf, cu_seqlens, n_seq, max_seqlen, aux=aux, sum_sq=sum_sq_seqlen)
+            return inter[k] if k is not None else None
+        self._run_layers(self.layers, resid, x_buf, qkv_buf, h_buf, cu_seqlens, n_seq, max_seqlen, sum_sq_seqlen,
+                         aux_of=aux_of)
         # layernorm_post + gated post-tile positional embedding, in place on the fp32 stream
         ops.layernorm(resid, *self.post_ln, enc.norm_eps, out=resid, out_f32=True, tile_add=self.post_tile_scaled,
                       tile_image=tile_image, image_table=image_ar, tile_slot=tile_slot, rows_per_tile=P + 1,
                       slots=self.slots)
-        for L in self.global_layers:
-            self._block(L, resid, x_buf, qkv_buf, h_buf, cu_seqlens, n_seq, max_seqlen, sum_sq=sum_sq_seqlen)
+        self._run_layers(self.global_layers, resid, x_buf, qkv_buf, h_buf, cu_seqlens, n_seq, max_seqlen,
+                         sum_sq_seqlen)
         del x_buf, qkv_buf, h_buf
         if out_alloc is not None:
             return ops.pack_mllama(resid, inter, out=out_alloc(T, d * (1 + len(outs))), peer=True)

@@ -156,9 +156,11 @@ def preprocess(src, src_off, w, h, tile_off, geom, n: int, total_tiles: int, spe
 
 
 def gemm(a: torch.Tensor, b: torch.Tensor, epilogue: int = EPI_BF16, bias=None, out=None, gate: float = 1.0,
-         aux=None):
+         aux=None, ln_stats_out=None, ln_mr=None, ln_c1=None):
     """out = epilogue(a @ b.T): a [M, K] bf16, b [N, K] bf16 (nn.Linear weight layout).  Operands
-    are checked (CUDA, dtype, unit inner stride) before the raw pointers cross the C ABI."""
+    are checked (CUDA, dtype, unit inner stride) before the raw pointers cross the C ABI.
+    LayerNorm fold (mmk_gemm_bf16_ln): ``ln_stats_out`` f32 [M, N/32, 2] from a RESID_F32 producer;
+    ``ln_mr`` f32 [M, 2] + ``ln_c1`` f32 [N] for a consumer whose ``b`` is W * gamma."""
     _need_rows(a, torch.bfloat16, "gemm a")
     _need_rows(b, torch.bfloat16, "gemm b")
     m, k = a.shape
@@ -180,11 +182,25 @@ def gemm(a: torch.Tensor, b: torch.Tensor, epilogue: int = EPI_BF16, bias=None, 
             raise SpecError(f"gemm: bias must be a contiguous CUDA float32 [{n}] tensor")
     if aux is not None:
         _need_rows(aux, torch.bfloat16, "gemm aux", n)
+    for t, nm, numel in ((ln_stats_out, "ln_stats_out", m * (n // 32) * 2), (ln_mr, "ln_mr", m * 2), (ln_c1, "ln_c1", n)):
+        if t is not None and (t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous() or t.numel() < numel):
+            raise SpecError(f"gemm: {nm} must be a contiguous CUDA float32 tensor of >= {numel} elements")
     _t0 = _begin()
-    _lib.check(_lib.lib.mmk_gemm_bf16(a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), m, n, k, epilogue,
-                                      _p(bias), out.data_ptr(), out.stride(0), float(gate), _p(aux),
-                                      aux.stride(0) if aux is not None else 0, _s()))
+    _lib.check(_lib.lib.mmk_gemm_bf16_ln(a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), m, n, k, epilogue,
+                                         _p(bias), out.data_ptr(), out.stride(0), float(gate), _p(aux),
+                                         aux.stride(0) if aux is not None else 0, _p(ln_stats_out), _p(ln_mr),
+                                         _p(ln_c1), _s()))
     _end(f'gemm.{EPI_NAMES[epilogue]}', 2.0 * m * n * k, _t0)
+    return out
+
+
+def ln_stats_finalize(stats, rows: int, d: int, eps: float, out=None):
+    """Folded LayerNorm: per-chunk (mean, M2) of the producer GEMM -> f32 [rows, 2] (mean, rstd)."""
+    if out is None:
+        out = torch.empty(rows, 2, dtype=torch.float32, device=stats.device)
+    _t0 = _begin()
+    _lib.check(_lib.lib.mmk_ln_stats_finalize(stats.data_ptr(), rows, d, float(eps), out.data_ptr(), _s()))
+    _end('layernorm', rows * (d // 32) * 8.0 + rows * 8.0, _t0)
     return out
 
 

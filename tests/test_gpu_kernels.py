@@ -465,3 +465,46 @@ def test_abi_status_codes_map_to_reference_exceptions(mk):
     # the context stays usable after every rejected call
     torch.cuda.synchronize()
     assert torch.equal(ops.pack_mllama(fin, inter[:1], peer=True), ops.pack_mllama(fin, inter[:1]))
+
+
+@pytest.mark.parametrize("m,d,n,epi", [(5000, 1280, 3840, 0), (5000, 1280, 5120, 1), (700, 768, 3072, 2),
+                                       (129, 1024, 4096, 2), (20011, 1280, 1280, 0)])
+def test_layernorm_folded_into_gemms(mk, m, d, n, epi):
+    """mmk_gemm_bf16_ln: a residual GEMM emitting the bf16 copy + per-chunk LN statistics, the
+    finalize kernel, and a consumer GEMM with W * gamma and the (mu, rstd) epilogue equal
+    LayerNorm -> GEMM in fp32 (both the CTA-pair kernel and the single-CTA kernel for small M)."""
+    _, ops, _ = mk
+    g = torch.Generator(device="cuda").manual_seed(m + n)
+    resid = torch.randn(m, d, device="cuda", generator=g) * 2 + 0.5
+    h = (torch.randn(m, 4 * 128, device="cuda", generator=g)).bfloat16()
+    w2 = (torch.randn(d, 4 * 128, device="cuda", generator=g) * 0.05).bfloat16()
+    b2 = torch.randn(d, device="cuda", generator=g) * 0.1
+    gamma = 1 + 0.2 * torch.randn(d, device="cuda", generator=g)
+    beta = 0.2 * torch.randn(d, device="cuda", generator=g)
+    w = (torch.randn(n, d, device="cuda", generator=g) * 0.05).bfloat16()
+    bias = torch.randn(n, device="cuda", generator=g) * 0.1
+    # reference: residual update, LayerNorm in fp32, GEMM in fp32
+    r_ref = resid + 0.7 * (h.float() @ w2.float().t() + b2)
+    x = torch.nn.functional.layer_norm(r_ref, (d,), gamma, beta, 1e-5)
+    ref = x @ w.float().t() + bias
+    if epi == 1:
+        ref = torch.nn.functional.gelu(ref)
+    elif epi == 2:
+        ref = ref * torch.sigmoid(1.702 * ref)
+    # folded path
+    xr = torch.empty(m, d, dtype=torch.bfloat16, device="cuda")
+    stats = torch.empty(m, d // 32, 2, device="cuda")
+    mr = torch.empty(m, 2, device="cuda")
+    r = resid.clone()
+    ops.gemm(h, w2, ops.EPI_RESID_F32, bias=b2, out=r, gate=0.7, aux=xr, ln_stats_out=stats)
+    ops.ln_stats_finalize(stats, m, d, 1e-5, out=mr)
+    torch.testing.assert_close(r, r_ref, rtol=1e-4, atol=1e-3)
+    mu, var = r_ref.mean(1), r_ref.var(1, unbiased=False)
+    torch.testing.assert_close(mr[:, 0], mu, rtol=1e-4, atol=1e-4)
+    torch.testing.assert_close(mr[:, 1], torch.rsqrt(var + 1e-5), rtol=1e-4, atol=1e-4)
+    wf = (w.double() * gamma.double()[None, :]).bfloat16()
+    c1 = wf.double().sum(1).float()
+    c2 = (w.double() @ beta.double() + bias.double()).float()
+    out = ops.gemm(xr, wf, epi, bias=c2, ln_mr=mr, ln_c1=c1)
+    rel = ((out.float() - ref).norm() / ref.norm()).item()
+    assert rel < 1e-2, rel
