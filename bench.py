@@ -82,6 +82,16 @@ def image_dims(spec, n_images: int, seed: int = 0, fixed=None):
     return dims[:n_images]
 
 
+def workload_dims(spec, wl, B, G, scaling):
+    """Image sizes of one step over all GPUs.  Weak scaling: the N=1 batch's sizes repeated per GPU
+    (new pixels for every copy), so the cost-balanced partition hands every rank the same work as
+    the one-GPU step; strong scaling: the first G generator images."""
+    if scaling == "weak":
+        base = image_dims(spec, B, fixed=wl.get("fixed"))
+        return [base[i % B] for i in range(G)]
+    return image_dims(spec, G, fixed=wl.get("fixed"))
+
+
 def make_images(dims, seed, first_index: int = 0):
     """Random uint8 pixels; image i of the workload is seeded by (seed, first_index + i), so an
     image has the same pixels whichever rank encodes it."""
@@ -266,7 +276,7 @@ def run_reference(args, spec, wl, rank, world, out=None):
     weights = init_weights(spec, 0)
     B = args.batch or wl["batch"]
     G = B * world if args.scaling == "weak" else (args.global_batch or 4 * B)
-    dims = image_dims(spec, G, fixed=wl.get("fixed"))
+    dims = workload_dims(spec, wl, B, G, args.scaling)
     ms = MixSampler(spec, dims, 1000)
     step_s = []
     for s_i in range(args.warmup + args.steps):
@@ -333,7 +343,7 @@ def main():
     # the step's images: weak scaling N x B (per-GPU work fixed), strong scaling a fixed global
     # batch; partitioned over the ranks by the path's own DP partition weighted by encoder FLOPs
     G = B * world if args.scaling == "weak" else (args.global_batch or 4 * B)
-    all_dims = image_dims(spec, G, fixed=wl.get("fixed"))
+    all_dims = workload_dims(spec, wl, B, G, args.scaling)
     all_tiles = [core.tile_count(w, h, spec) for w, h in all_dims]
     shards = partition_images(all_tiles, world, costs=[encoder_flops(spec, [t]) for t in all_tiles])
     mine = shards[rank]
