@@ -116,8 +116,10 @@ def encoder_flops(spec, tiles_list):
     d, ff = enc.hidden, enc.ffn
     tot = 0.0
     for t in tiles_list:
-        S = t * (P + 1)
-        tot += L * S * (8 * d * d + 4 * d * ff) + 4 * L * S * S * d + t * P * 2 * (3 * enc.patch_px ** 2) * d
+        S = t * spec.seq_per_tile
+        # attention span: the whole image (Mllama), one tile (CLIP-family ViTs)
+        attn = S * S if enc.family == "mllama" else t * spec.seq_per_tile ** 2
+        tot += L * S * (8 * d * d + 4 * d * ff) + 4 * L * attn * d + t * P * 2 * (3 * enc.patch_px ** 2) * d
     return tot
 
 

@@ -43,7 +43,8 @@ enum mmk_epilogue {
   MMK_EPI_BF16_GELU = 1,      /* out bf16 = gelu_erf(acc + bias)     (Mllama FC1)   */
   MMK_EPI_BF16_QUICKGELU = 2, /* out bf16 = quick_gelu(acc + bias)   (CLIP FC1)     */
   MMK_EPI_F32 = 3,            /* out f32  = acc + bias               (patch embed)  */
-  MMK_EPI_RESID_F32 = 4       /* out f32 += gate * (acc + bias); aux bf16 = out     */
+  MMK_EPI_RESID_F32 = 4,      /* out f32 += gate * (acc + bias); aux bf16 = out     */
+  MMK_EPI_BF16_GELU_TANH = 5  /* out bf16 = gelu_tanh(acc + bias)    (SigLIP FC1)   */
 };
 
 const char* mmk_version(void);
@@ -75,7 +76,8 @@ int mmk_tile_index(const int64_t* tile_off, int32_t n, int32_t* tile_image, int3
 
 /* Attention sequence offsets of the varlen attention (one sequence per image):
  * cu_seqlens[i] = tile_off[i] * seq_per_tile for i in [0, n] (int32; seq_per_tile = patches per
- * tile + 1 class token).  Total sequence rows must stay below 2^31. */
+ * tile + class token); tile_off NULL: cu_seqlens[i] = i * seq_per_tile (one sequence per tile, n =
+ * tiles).  Total sequence rows must stay below 2^31. */
 int mmk_seq_offsets(const int64_t* tile_off, int32_t n, int32_t seq_per_tile, int32_t* cu_seqlens,
                     cudaStream_t stream);
 

@@ -34,6 +34,8 @@ def _ln(x, w, b, eps):
 def _act(x, act):
     if act == "gelu":
         return Fn.gelu(x)
+    if act == "gelu_tanh":  # gelu_pytorch_tanh (SigLIP)
+        return Fn.gelu(x, approximate="tanh")
     return x * torch.sigmoid(1.702 * x)
 
 
@@ -65,23 +67,27 @@ def _layer(h, W, pre, heads, act, eps, gated=False, mask=None):
 
 
 def patch_embed(patches: torch.Tensor, W) -> torch.Tensor:
-    """patches [n, k_pad] (float32 view of the bf16 patch matrix) -> [n, d]."""
+    """patches [n, k_pad] (float32 view of the bf16 patch matrix) -> [n, d] (+ the conv bias)."""
     k = W["patch_w"].shape[1]
-    return patches[:, :k].float() @ W["patch_w"].t()
+    x = patches[:, :k].float() @ W["patch_w"].t()
+    return x + W["patch_b"] if W.get("patch_b") is not None else x
 
 
 def clip_image(patches: torch.Tensor, W, enc) -> torch.Tensor:
-    """One single-tile image: patches [P, k_pad] -> emitted tokens [P + 1 - drop_cls, d]."""
+    """One single-tile image: patches [P, k_pad] -> emitted tokens [P + cls - drop_cls, d].
+    SigLIP (modeling_siglip.py: SiglipVisionEmbeddings, no class token, no pre-LN, conv bias,
+    gelu_pytorch_tanh) is the same family with cls_token / pre_ln off."""
     eps = enc.norm_eps
     x = patch_embed(patches, W)
-    h = torch.cat([W["cls"][None], x], 0) + W["pos"]
-    h = _ln(h, W["pre_ln_w"], W["pre_ln_b"], eps)
+    h = (torch.cat([W["cls"][None], x], 0) if getattr(enc, "cls_token", True) else x) + W["pos"]
+    if getattr(enc, "pre_ln", True):
+        h = _ln(h, W["pre_ln_w"], W["pre_ln_b"], eps)
     n_run = enc.layers if enc.out_layer == -1 else enc.layers + 1 + enc.out_layer
     for i in range(n_run):
         h = _layer(h, W, f"l{i}.", enc.heads, enc.act, eps)
     # hidden_states[out_layer] of CLIPVisionModel: post_layernorm is applied to the pooled CLS
     # only (modeling_clip.py), never to the emitted sequence
-    return h[1:] if enc.drop_cls else h
+    return h[1:] if getattr(enc, "drop_cls", False) else h
 
 
 def mllama_image(patches: torch.Tensor, W, enc, ar_id: int, n_tiles: int) -> torch.Tensor:

@@ -81,8 +81,8 @@ void oracle_preprocess(const uint8_t* src, const int64_t* src_off, int chw, cons
       if (is_thumb) { rw = T; rh = T; }
       else if (mode == 0) { ox = (t % cols) * T; oy = (t / cols) * T; clip = 1; }
       else { ox = (nw - T) / 2; oy = (nh - T) / 2; }
-      for (yy = 0; yy < T; ++yy) {
-        for (xx = 0; xx < T; ++xx) {
+      for (yy = 0; yy < ps * p; ++yy) {    /* the patch grid: floor(T / p) patches per side */
+        for (xx = 0; xx < ps * p; ++xx) {
           const int X = ox + xx, Y = oy + yy;
           const int64_t patch = (tile_off[i] + t) * (int64_t)ps * ps + (yy / p) * ps + (xx / p);
           int c;

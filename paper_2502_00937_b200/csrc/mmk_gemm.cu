@@ -62,6 +62,16 @@ MMK_DEV float quick_gelu(float x) {
   return x * r;
 }
 
+// tanh-approximated GELU (gelu_pytorch_tanh, SigLIP): 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3)))
+// with tanh as 1 - 2 / (1 + e^{2u}) (one MUFU ex2, one MUFU rcp); saturates cleanly at +-inf.
+MMK_DEV float gelu_tanh(float x) {
+  const float u = 0.7978845608028654f * fmaf(0.044715f * x, x * x, x);
+  float e, r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(2.8853900817779268f * u));  // e^{2u} = 2^{2u log2 e}
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
+  return 0.5f * x * (2.0f - 2.0f * r);  // 1 + tanh(u) = 2 - 2 / (1 + e^{2u})
+}
+
 // Paired forms (FFMA2 / FMUL2 on the FMA pipe, half the issue slots; same math as above).
 MMK_DEV float2 gelu_erf2(float2 x) {
   const float2 z = __fmul2_rn(make_float2(fabsf(x.x), fabsf(x.y)), make_float2(0.70710678118654752f, 0.70710678118654752f));
@@ -87,6 +97,7 @@ template <int EPI>
 MMK_DEV float2 apply_act2(float2 v) {
   if constexpr (EPI == MMK_EPI_BF16_GELU) return gelu_erf2(v);
   else if constexpr (EPI == MMK_EPI_BF16_QUICKGELU) return make_float2(quick_gelu(v.x), quick_gelu(v.y));
+  else if constexpr (EPI == MMK_EPI_BF16_GELU_TANH) return make_float2(gelu_tanh(v.x), gelu_tanh(v.y));
   else return v;
 }
 
@@ -94,6 +105,7 @@ template <int EPI>
 MMK_DEV float apply_act(float v) {
   if constexpr (EPI == MMK_EPI_BF16_GELU) return gelu_erf(v);
   else if constexpr (EPI == MMK_EPI_BF16_QUICKGELU) return quick_gelu(v);
+  else if constexpr (EPI == MMK_EPI_BF16_GELU_TANH) return gelu_tanh(v);
   else return v;
 }
 
@@ -501,7 +513,8 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
     }
   } else if (warp >= 4) {
     // ------------------------------------------------ epilogue (both CTAs, own 128 rows)
-    constexpr bool kTmaStore = EPI == MMK_EPI_BF16 || EPI == MMK_EPI_BF16_GELU || EPI == MMK_EPI_BF16_QUICKGELU;
+    constexpr bool kTmaStore = EPI == MMK_EPI_BF16 || EPI == MMK_EPI_BF16_GELU || EPI == MMK_EPI_BF16_QUICKGELU ||
+                               EPI == MMK_EPI_BF16_GELU_TANH;
     const uint32_t q = warp & 3;
     const uint32_t half = (warp - 4) >> 2;
     constexpr int kColsPerWarp = BN / 2;
@@ -726,6 +739,7 @@ static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, i
     case MMK_EPI_BF16: return launch_gemm<BN, STAGES, MMK_EPI_BF16>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
     case MMK_EPI_BF16_GELU: return launch_gemm<BN, STAGES, MMK_EPI_BF16_GELU>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
     case MMK_EPI_BF16_QUICKGELU: return launch_gemm<BN, STAGES, MMK_EPI_BF16_QUICKGELU>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
+    case MMK_EPI_BF16_GELU_TANH: return launch_gemm<BN, STAGES, MMK_EPI_BF16_GELU_TANH>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
     case MMK_EPI_F32: return launch_gemm<BN, STAGES, MMK_EPI_F32>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
     case MMK_EPI_RESID_F32: return launch_gemm<BN, STAGES, MMK_EPI_RESID_F32>(ta, tb, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
     default: return set_error(MMK_ERR_ARG, "gemm: unknown epilogue %d", epi);
@@ -760,6 +774,7 @@ static int dispatch_epi_2sm(int epi, const CUtensorMap& ta, const CUtensorMap& t
     case MMK_EPI_BF16: return launch_gemm_2sm<STAGES, MMK_EPI_BF16>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
     case MMK_EPI_BF16_GELU: return launch_gemm_2sm<STAGES, MMK_EPI_BF16_GELU>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
     case MMK_EPI_BF16_QUICKGELU: return launch_gemm_2sm<STAGES, MMK_EPI_BF16_QUICKGELU>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
+    case MMK_EPI_BF16_GELU_TANH: return launch_gemm_2sm<STAGES, MMK_EPI_BF16_GELU_TANH>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
     case MMK_EPI_F32: return launch_gemm_2sm<STAGES, MMK_EPI_F32>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
     case MMK_EPI_RESID_F32:
       // the fp32 residual streams through shared memory by TMA (O-proj 0.420 -> 0.365 ms, FC2

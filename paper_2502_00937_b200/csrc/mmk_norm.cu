@@ -100,10 +100,12 @@ embed_kernel(const float* __restrict__ patch_out, const int32_t* __restrict__ ti
   griddep_launch_dependents();
   const int lane = threadIdx.x & 31;
   const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-  const int64_t rows = static_cast<int64_t>(total_tiles) * (P + 1);
+  const int C = cls != nullptr ? 1 : 0;  // SigLIP-style encoders have no class token
+  const int S = P + C;                   // tokens per tile
+  const int64_t rows = static_cast<int64_t>(total_tiles) * S;
   if (row >= rows) return;
-  const int g = static_cast<int>(row / (P + 1));
-  const int p = static_cast<int>(row - static_cast<int64_t>(g) * (P + 1));
+  const int g = static_cast<int>(row / S);
+  const int p = static_cast<int>(row - static_cast<int64_t>(g) * S);
   const int ar = image_ar ? image_ar[tile_image[g]] : 0;
   const int slot = tile_slot ? tile_slot[g] : 0;
   float4 v[VEC];
@@ -111,10 +113,10 @@ embed_kernel(const float* __restrict__ patch_out, const int32_t* __restrict__ ti
   for (int j = 0; j < VEC; ++j) {
     const int col = lane * 4 + j * 128;
     float4 a;
-    if (p == 0) {
+    if (C && p == 0) {
       a = __ldg(reinterpret_cast<const float4*>(cls + col));
     } else {
-      a = *reinterpret_cast<const float4*>(patch_out + (static_cast<int64_t>(g) * P + (p - 1)) * d + col);
+      a = *reinterpret_cast<const float4*>(patch_out + (static_cast<int64_t>(g) * P + (p - C)) * d + col);
       if (pre_tile != nullptr) {
         const float4 t = __ldg(reinterpret_cast<const float4*>(pre_tile + (static_cast<int64_t>(ar) * slots + slot) * d + col));
         a.x += pre_scale * t.x; a.y += pre_scale * t.y; a.z += pre_scale * t.z; a.w += pre_scale * t.w;
@@ -124,12 +126,12 @@ embed_kernel(const float* __restrict__ patch_out, const int32_t* __restrict__ ti
     a.x += pos_scale * ps.x; a.y += pos_scale * ps.y; a.z += pos_scale * ps.z; a.w += pos_scale * ps.w;
     if (tile_pos != nullptr) {
       const float4 t = __ldg(reinterpret_cast<const float4*>(
-          tile_pos + ((static_cast<int64_t>(ar) * slots + slot) * (P + 1) + p) * d + col));
+          tile_pos + ((static_cast<int64_t>(ar) * slots + slot) * S + p) * d + col));
       a.x += tile_pos_scale * t.x; a.y += tile_pos_scale * t.y; a.z += tile_pos_scale * t.z; a.w += tile_pos_scale * t.w;
     }
     v[j] = a;
   }
-  ln_inplace<VEC>(v, d, gamma, beta, eps, lane);
+  if (gamma != nullptr) ln_inplace<VEC>(v, d, gamma, beta, eps, lane);  // no LN_pre: SigLIP
   store_row<VEC>(resid, 1, row, d, v, lane);
 }
 
@@ -336,6 +338,7 @@ extern "C" int mmk_layernorm(const float* x, void* y, int32_t y_f32, int32_t row
   switch (d / 128 * (d % 128 == 0)) {
     MMK_LN_CASE(4)
     MMK_LN_CASE(6)
+    MMK_LN_CASE(9)
     MMK_LN_CASE(8)
     MMK_LN_CASE(10)
     MMK_LN_CASE(12)
@@ -363,10 +366,11 @@ extern "C" int mmk_embed_tokens(const float* patch_out, const int32_t* tile_imag
   if (total_tiles < 0 || patches_per_tile <= 0 || d <= 0) return set_error(MMK_ERR_ARG, "embed: bad shape");
   if ((tile_pos || pre_tile) && (!tile_image || !tile_slot || !image_ar))
     return set_error(MMK_ERR_ARG, "embed: tile embeddings need tile_image/tile_slot/image_ar");
-  const int64_t rows = static_cast<int64_t>(total_tiles) * (patches_per_tile + 1);
+  const int64_t rows = static_cast<int64_t>(total_tiles) * (patches_per_tile + (cls != nullptr ? 1 : 0));
   if (rows == 0) return MMK_OK;
   switch (d / 128 * (d % 128 == 0)) {
     MMK_EMB_CASE(4)
+    MMK_EMB_CASE(9)
     MMK_EMB_CASE(6)
     MMK_EMB_CASE(8)
     MMK_EMB_CASE(10)

@@ -197,13 +197,14 @@ __global__ void tile_index_kernel(const int64_t* __restrict__ tile_off, int n, i
 }
 
 // int32 attention offsets cu_seqlens[i] = tile_off[i] * seq_per_tile (i <= n): the sequences of
-// the varlen attention are whole images (all tiles of an image attend to each other).
+// the varlen attention are whole images (Mllama: all tiles of an image attend to each other);
+// tile_off == NULL gives one sequence per tile (CLIP-family encoders see each tile alone).
 __global__ void seq_offsets_kernel(const int64_t* __restrict__ tile_off, int n, int seq_per_tile,
                                    int32_t* __restrict__ cu_seqlens) {
   griddep_wait();  // PDL: inputs come from the preceding kernel
   griddep_launch_dependents();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i <= n) cu_seqlens[i] = static_cast<int32_t>(tile_off[i] * seq_per_tile);
+  if (i <= n) cu_seqlens[i] = static_cast<int32_t>((tile_off ? tile_off[i] : i) * seq_per_tile);
 }
 
 }  // namespace mmk

@@ -396,7 +396,9 @@ extern "C" int mmk_preprocess(const uint8_t* src, const int64_t* src_off, int32_
                               int32_t tile_px, int32_t patch_px, int32_t k_pad, int32_t mode, int32_t thumbnail,
                               const float* scale3, const float* shift3, void* patches, cudaStream_t stream) {
   if (n < 0 || total_tiles < 0) return set_error(MMK_ERR_ARG, "preprocess: negative sizes");
-  if (patch_px < 1 || tile_px % patch_px != 0) return set_error(MMK_ERR_ARG, "preprocess: tile_px %% patch_px != 0");
+  // the patch grid is floor(tile_px / patch_px) per side (SigLIP 384 / 14 -> 27, trailing pixels unused,
+  // as a stride-p "valid" convolution)
+  if (patch_px < 1 || tile_px < patch_px) return set_error(MMK_ERR_ARG, "preprocess: tile_px < patch_px");
   if (patch_px > kMaxPatch) return set_error(MMK_ERR_UNSUPPORTED, "preprocess: patch_px %d > %d", patch_px, kMaxPatch);
   if (patch_px % 2) return set_error(MMK_ERR_UNSUPPORTED, "preprocess: odd patch_px %d", patch_px);
   if (k_pad < 3 * patch_px * patch_px || k_pad % 8 != 0) return set_error(MMK_ERR_ARG, "preprocess: bad k_pad");

@@ -37,14 +37,22 @@ class DeviceEncoder:
         enc = spec.encoder
         if enc is None:
             raise SpecError(f"{spec.name}: no encoder block")
-        if enc.head_dim not in (64, 80):
+        if enc.head_dim > 80:
             from ._lib import ProfileError
             raise ProfileError(f"{spec.name}: head_dim {enc.head_dim} not supported by the attention kernel")
         self.spec, self.enc, self.device = spec, enc, torch.device(device)
+        # head_dim below a kernel size (SigLIP 72) runs as zero-padded heads of the next size (80):
+        # zero Q/K columns leave the scores unchanged (scale stays head_dim^-0.5), zero V columns
+        # give zero output columns, which meet zero columns of the O-projection
+        self.hd = enc.head_dim
+        self.hd_pad = 64 if enc.head_dim <= 64 else 80
+        # FFN widths that are not a multiple of 256 (SigLIP 4304) pad with zero units (act(0) = 0)
+        self.ffn_pad = -(-enc.ffn // 256) * 256 if enc.ffn % 256 else enc.ffn
         # LayerNorm folded into the GEMMs (mmk_gemm_bf16_ln): every LN whose input comes from a
         # residual GEMM; MMK_LN_FOLD=0 runs the separate LayerNorm kernel instead (A/B runs)
         self.fold_ln = (os.environ.get("MMK_LN_FOLD", "1") != "0") if fold_ln is None else fold_ln
         self.P = (spec.tile_edge_px // enc.patch_px) ** 2
+        self.S = self.P + int(enc.cls_token)  # encoder tokens per tile
         self.k_pad = k_pad_of(spec)
         dev = self.device
         bf = lambda t: t.to(dev, torch.bfloat16).contiguous()  # noqa: E731
@@ -53,8 +61,9 @@ class DeviceEncoder:
         pw = torch.zeros(d, self.k_pad)
         pw[:, :weights["patch_w"].shape[1]] = weights["patch_w"]
         self.patch_w = bf(pw)
-        self.cls, self.pos = f32(weights["cls"]), f32(weights["pos"])
-        self.pre_ln = (f32(weights["pre_ln_w"]), f32(weights["pre_ln_b"]))
+        self.patch_b = f32(weights.get("patch_b"))
+        self.cls, self.pos = f32(weights.get("cls")), f32(weights["pos"])
+        self.pre_ln = (f32(weights["pre_ln_w"]), f32(weights["pre_ln_b"])) if enc.pre_ln else (None, None)
         self.post_ln = (f32(weights["post_ln_w"]), f32(weights["post_ln_b"]))
 
         def folded(w, g, b, bias):
@@ -65,22 +74,53 @@ class DeviceEncoder:
             c2 = w.double() @ b.double() + (bias.double() if bias is not None else 0.0)
             return bf(wf), f32(c1.float()), f32(c2.float())
 
+        H, hd, hdp, ff, ffp = enc.heads, self.hd, self.hd_pad, enc.ffn, self.ffn_pad
+
+        def pad_heads_rows(w):  # [3*H*hd, ...] -> [3*H*hdp, ...] (zero rows per head)
+            if w is None or hd == hdp:
+                return w
+            v = w.reshape(3, H, hd, *w.shape[1:])
+            out = torch.zeros(3, H, hdp, *w.shape[1:], dtype=w.dtype)
+            out[:, :, :hd] = v
+            return out.reshape(3 * H * hdp, *w.shape[1:])
+
+        def pad_heads_cols(w):  # [d, H*hd] -> [d, H*hdp]
+            if hd == hdp:
+                return w
+            out = torch.zeros(w.shape[0], H, hdp, dtype=w.dtype)
+            out[:, :, :hd] = w.reshape(w.shape[0], H, hd)
+            return out.reshape(w.shape[0], H * hdp)
+
+        def pad_ffn_rows(w):  # [ff, ...] -> [ffp, ...]
+            if w is None or ff == ffp:
+                return w
+            out = torch.zeros(ffp, *w.shape[1:], dtype=w.dtype)
+            out[:ff] = w
+            return out
+
+        def pad_ffn_cols(w):  # [d, ff] -> [d, ffp]
+            if ff == ffp:
+                return w
+            out = torch.zeros(w.shape[0], ffp, dtype=w.dtype)
+            out[:, :ff] = w
+            return out
+
         def block(pre, gated):
+            qkv_w, qkv_b = pad_heads_rows(weights[pre + "qkv_w"]), pad_heads_rows(weights.get(pre + "qkv_b"))
+            fc1_w, fc1_b = pad_ffn_rows(weights[pre + "fc1_w"]), pad_ffn_rows(weights[pre + "fc1_b"])
             L = {
                 "ln1": (f32(weights[pre + "ln1_w"]), f32(weights[pre + "ln1_b"])),
-                "qkv_w": bf(weights[pre + "qkv_w"]), "qkv_b": f32(weights.get(pre + "qkv_b")),
-                "o_w": bf(weights[pre + "o_w"]), "o_b": f32(weights.get(pre + "o_b")),
+                "qkv_w": bf(qkv_w), "qkv_b": f32(qkv_b),
+                "o_w": bf(pad_heads_cols(weights[pre + "o_w"])), "o_b": f32(weights.get(pre + "o_b")),
                 "ln2": (f32(weights[pre + "ln2_w"]), f32(weights[pre + "ln2_b"])),
-                "fc1_w": bf(weights[pre + "fc1_w"]), "fc1_b": f32(weights[pre + "fc1_b"]),
-                "fc2_w": bf(weights[pre + "fc2_w"]), "fc2_b": f32(weights[pre + "fc2_b"]),
+                "fc1_w": bf(fc1_w), "fc1_b": f32(fc1_b),
+                "fc2_w": bf(pad_ffn_cols(weights[pre + "fc2_w"])), "fc2_b": f32(weights[pre + "fc2_b"]),
                 "gate_attn": math.tanh(float(weights[pre + "gate_attn"])) if gated else 1.0,
                 "gate_ffn": math.tanh(float(weights[pre + "gate_ffn"])) if gated else 1.0,
             }
             if self.fold_ln:
-                L["qkv_f"] = folded(weights[pre + "qkv_w"], weights[pre + "ln1_w"], weights[pre + "ln1_b"],
-                                    weights.get(pre + "qkv_b"))
-                L["fc1_f"] = folded(weights[pre + "fc1_w"], weights[pre + "ln2_w"], weights[pre + "ln2_b"],
-                                    weights[pre + "fc1_b"])
+                L["qkv_f"] = folded(qkv_w, weights[pre + "ln1_w"], weights[pre + "ln1_b"], qkv_b)
+                L["fc1_f"] = folded(fc1_w, weights[pre + "ln2_w"], weights[pre + "ln2_b"], fc1_b)
             return L
 
         self.layers = [block(f"l{i}.", False) for i in range(enc.layers)]
@@ -101,7 +141,7 @@ class DeviceEncoder:
 
     # ------------------------------------------------------------------ layers
     def _block(self, L, resid, x_buf, qkv_buf, h_buf, cu, n_seq, max_s, aux=None, sum_sq=0.0, ln=None, xr=None,
-               stats_next=False):
+               stats_next=False, a_buf=None):
         """One pre-LN block.  Folded LayerNorms (self.fold_ln): ``ln`` = (stats, mr) buffers; LN1
         is folded when ``xr`` (the bf16 copy of the residual the previous FC2 wrote) is given, LN2
         always; with ``stats_next`` the FC2 also emits the next block's LN statistics.  Returns the
@@ -114,18 +154,20 @@ class DeviceEncoder:
         else:
             ops.layernorm(resid, *L["ln1"], enc.norm_eps, out=x_buf)
             ops.gemm(x_buf, L["qkv_w"], ops.EPI_BF16, bias=L["qkv_b"], out=qkv_buf)
-        ops.attention(qkv_buf, cu, n_seq, max_s, enc.heads, enc.head_dim, out=x_buf, sum_sq_seqlen=sum_sq)
+        a_buf = x_buf if a_buf is None else a_buf  # attention output (H * padded head_dim columns)
+        ops.attention(qkv_buf, cu, n_seq, max_s, enc.heads, self.hd_pad, out=a_buf, scale=self.hd ** -0.5,
+                      sum_sq_seqlen=sum_sq * self.hd / self.hd_pad)
         if ln is not None:
             # the O-proj writes the residual's bf16 copy into the (now free) Q columns of qkv_buf
             # and its LN statistics; FC1 consumes the copy with LN2 folded in
             xr2 = qkv_buf[:, :d]
-            ops.gemm(x_buf, L["o_w"], ops.EPI_RESID_F32, bias=L["o_b"], out=resid, gate=L["gate_attn"], aux=xr2,
+            ops.gemm(a_buf, L["o_w"], ops.EPI_RESID_F32, bias=L["o_b"], out=resid, gate=L["gate_attn"], aux=xr2,
                      ln_stats_out=ln[0])
             ops.ln_stats_finalize(ln[0], T, d, enc.norm_eps, out=ln[1])
             wf, c1, c2 = L["fc1_f"]
             ops.gemm(xr2, wf, ops.ACT_EPI[enc.act], bias=c2, out=h_buf, ln_mr=ln[1], ln_c1=c1)
         else:
-            ops.gemm(x_buf, L["o_w"], ops.EPI_RESID_F32, bias=L["o_b"], out=resid, gate=L["gate_attn"])
+            ops.gemm(a_buf, L["o_w"], ops.EPI_RESID_F32, bias=L["o_b"], out=resid, gate=L["gate_attn"])
             ops.layernorm(resid, *L["ln2"], enc.norm_eps, out=x_buf)
             ops.gemm(x_buf, L["fc1_w"], ops.ACT_EPI[enc.act], bias=L["fc1_b"], out=h_buf)
         if ln is not None and stats_next:
@@ -142,6 +184,9 @@ class DeviceEncoder:
     def _run_layers(self, layers, resid, x_buf, qkv_buf, h_buf, cu, n_seq, max_s, sum_sq, aux_of=lambda i: None):
         """A stack of blocks; with fold_ln only the stack's first LN1 runs as a LayerNorm kernel."""
         T, d = resid.shape
+        a_buf = None
+        if self.enc.heads * self.hd_pad != d:  # padded heads: the attention output is wider than d
+            a_buf = torch.empty(T, self.enc.heads * self.hd_pad, dtype=torch.bfloat16, device=resid.device)
         ln = None
         if self.fold_ln and d % 32 == 0:
             ln = (torch.empty(T, d // 32, 2, dtype=torch.float32, device=resid.device),
@@ -149,7 +194,7 @@ class DeviceEncoder:
         xr = None
         for i, L in enumerate(layers):
             xr = self._block(L, resid, x_buf, qkv_buf, h_buf, cu, n_seq, max_s, aux=aux_of(i), sum_sq=sum_sq, ln=ln,
-                             xr=xr, stats_next=i + 1 < len(layers))
+                             xr=xr, stats_next=i + 1 < len(layers), a_buf=a_buf)
 
     def forward(self, patches: torch.Tensor, total_tiles: int, cu_seqlens: torch.Tensor, n_seq: int, max_seqlen: int,
                 tile_image=None, tile_slot=None, image_ar=None, out_alloc=None, sum_sq_seqlen: float = 0.0) -> torch.Tensor:
@@ -157,10 +202,10 @@ class DeviceEncoder:
         cu_seqlens int32 [n_seq+1] token offsets of the attention sequences (one per image).
         out_alloc(rows, width) -> bf16 tensor: destination of the packed output, possibly in the
         LLM-backend GPU's memory (peer view); the pack then streams whole rows over NVLink."""
-        enc, P, d = self.enc, self.P, self.enc.hidden
+        enc, P, d, S = self.enc, self.P, self.enc.hidden, self.S
         dev = patches.device
-        T = total_tiles * (P + 1)
-        patch_out = ops.gemm(patches, self.patch_w, ops.EPI_F32)
+        T = total_tiles * S
+        patch_out = ops.gemm(patches, self.patch_w, ops.EPI_F32, bias=self.patch_b)
         if enc.family == "mllama":
             resid = ops.embed_tokens(patch_out, total_tiles, P, self.cls, self.pos, self.pos_scale, *self.pre_ln,
                                      enc.norm_eps, tile_image=tile_image, tile_slot=tile_slot, image_ar=image_ar,
@@ -170,8 +215,8 @@ class DeviceEncoder:
             resid = ops.embed_tokens(patch_out, total_tiles, P, self.cls, self.pos, 1.0, *self.pre_ln, enc.norm_eps)
         del patch_out
         x_buf = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
-        qkv_buf = torch.empty(T, 3 * d, dtype=torch.bfloat16, device=dev)
-        h_buf = torch.empty(T, enc.ffn, dtype=torch.bfloat16, device=dev)
+        qkv_buf = torch.empty(T, 3 * enc.heads * self.hd_pad, dtype=torch.bfloat16, device=dev)
+        h_buf = torch.empty(T, self.ffn_pad, dtype=torch.bfloat16, device=dev)
         if enc.family == "clip":
             n_run = enc.layers if enc.out_layer == -1 else enc.layers + 1 + enc.out_layer
             self._run_layers(self.layers[:n_run], resid, x_buf, qkv_buf, h_buf, cu_seqlens, n_seq, max_seqlen,
@@ -179,8 +224,8 @@ class DeviceEncoder:
             # emitted = hidden_states[out_layer] as transformers' CLIPVisionModel numbers them
             # (modeling_clip.py: post_layernorm touches only the pooled CLS, never the sequence)
             drop = 1 if enc.drop_cls else 0
-            dst = out_alloc(total_tiles * (P + 1 - drop), d) if out_alloc is not None else None
-            return ops.pack_drop_cls(resid, total_tiles, P + 1, drop, out=dst)
+            dst = out_alloc(total_tiles * (S - drop), d) if out_alloc is not None else None
+            return ops.pack_drop_cls(resid, total_tiles, S, drop, out=dst)
         # ---------------- mllama
         # intermediate capture: the FC2 epilogue of the layer whose output is the requested hidden
         # state writes a bf16 copy (EncoderSpec.out_layers_of: Meta "input of layer i" or

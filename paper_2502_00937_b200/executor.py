@@ -221,16 +221,23 @@ class ImagePathExecutor:
                                  total_tiles, spec, self.encoder.k_pad, self.encoder.norm_scale,
                                  self.encoder.norm_shift, chw=batch.chw, src_bytes=batch.src_bytes)
         # attention sequences: all tokens of one image (images never attend to each other)
-        seq_len = np.asarray(tiles, np.float64) * (P + 1)
-        cu = ops.seq_offsets(plan["tile_off"], n, P + 1)  # device-side: capturable in a CUDA graph
+        S = spec.seq_per_tile  # encoder tokens per tile (patches + class token if any)
+        if enc.family == "mllama":  # an image's tiles attend to each other
+            seq_len = np.asarray(tiles, np.float64) * S
+            cu = ops.seq_offsets(plan["tile_off"], n, S)  # device-side: capturable in a CUDA graph
+            n_seq, max_s = n, int(max(tiles)) * S
+        else:  # CLIP-family ViTs see every tile alone (multi-tile LLaVA-OV / thumbnails)
+            seq_len = np.full(total_tiles, float(S))
+            cu = ops.seq_offsets(None, total_tiles, S, device=self.device)
+            n_seq, max_s = total_tiles, S
         sum_sq = float(np.sum(seq_len ** 2))
-        max_s = int(max(tiles)) * (P + 1)
         if enc.family == "mllama":
             tile_image, tile_slot = ops.tile_index(plan["tile_off"], n, total_tiles)
-            emb = self.encoder.forward(patches, total_tiles, cu, n, max_s, tile_image, tile_slot, plan["ar_id"],
+            emb = self.encoder.forward(patches, total_tiles, cu, n_seq, max_s, tile_image, tile_slot, plan["ar_id"],
                                        out_alloc=out_alloc, sum_sq_seqlen=sum_sq)
         else:
-            emb = self.encoder.forward(patches, total_tiles, cu, n, max_s, out_alloc=out_alloc, sum_sq_seqlen=sum_sq)
+            emb = self.encoder.forward(patches, total_tiles, cu, n_seq, max_s, out_alloc=out_alloc,
+                                       sum_sq_seqlen=sum_sq)
         return PackedBatch(embeds=emb, tok_offsets=plan["tok_off"], tiles=tiles,
                            image_tokens=[t * spec.tokens_per_tile for t in tiles])
 

@@ -13,10 +13,10 @@ import torch
 from . import _lib
 from .core import SpecError
 
-EPI_BF16, EPI_BF16_GELU, EPI_BF16_QUICKGELU, EPI_F32, EPI_RESID_F32 = range(5)
-ACT_EPI = {"gelu": EPI_BF16_GELU, "quick_gelu": EPI_BF16_QUICKGELU}
+EPI_BF16, EPI_BF16_GELU, EPI_BF16_QUICKGELU, EPI_F32, EPI_RESID_F32, EPI_BF16_GELU_TANH = range(6)
+ACT_EPI = {"gelu": EPI_BF16_GELU, "quick_gelu": EPI_BF16_QUICKGELU, "gelu_tanh": EPI_BF16_GELU_TANH}
 EPI_NAMES = {EPI_BF16: "bf16", EPI_BF16_GELU: "gelu", EPI_BF16_QUICKGELU: "quickgelu", EPI_F32: "f32",
-             EPI_RESID_F32: "resid"}
+             EPI_RESID_F32: "resid", EPI_BF16_GELU_TANH: "gelutanh"}
 
 
 class LaunchLog:
@@ -127,12 +127,15 @@ def tile_index(tile_off: torch.Tensor, n: int, total_tiles: int):
     return tile_image, tile_slot
 
 
-def seq_offsets(tile_off: torch.Tensor, n: int, seq_per_tile: int):
-    """int32 cu_seqlens [n+1] of the per-image attention sequences (one kernel, graph-capturable)."""
-    _need(tile_off, torch.int64, "tile_off")
-    cu = torch.empty(n + 1, dtype=torch.int32, device=tile_off.device)
+def seq_offsets(tile_off: torch.Tensor | None, n: int, seq_per_tile: int, device=None):
+    """int32 cu_seqlens [n+1] of the attention sequences: whole images (from ``tile_off``) or, with
+    ``tile_off=None``, one sequence per tile (n = tiles).  One kernel, graph-capturable."""
+    if tile_off is not None:
+        _need(tile_off, torch.int64, "tile_off")
+        device = tile_off.device
+    cu = torch.empty(n + 1, dtype=torch.int32, device=device)
     _t0 = _begin()
-    _lib.check(_lib.lib.mmk_seq_offsets(tile_off.data_ptr(), n, seq_per_tile, cu.data_ptr(), _s()))
+    _lib.check(_lib.lib.mmk_seq_offsets(_p(tile_off), n, seq_per_tile, cu.data_ptr(), _s()))
     _end('tile_index', 0, _t0)
     return cu
 
@@ -247,15 +250,17 @@ def attention(qkv, cu_seqlens, n_seq: int, max_seqlen: int, heads: int, head_dim
 def embed_tokens(patch_out, total_tiles: int, patches_per_tile: int, cls, pos, pos_scale: float, gamma, beta,
                  eps: float, tile_image=None, tile_slot=None, image_ar=None, tile_pos=None,
                  tile_pos_scale: float = 0.0, pre_tile=None, pre_scale: float = 0.0, slots: int = 0, out=None):
+    """Token rows of every tile (class token when ``cls`` is given, patches + position terms),
+    LayerNorm'd when ``gamma`` is given (no LN_pre: SigLIP)."""
     d = patch_out.shape[1]
-    rows = total_tiles * (patches_per_tile + 1)
+    rows = total_tiles * (patches_per_tile + (1 if cls is not None else 0))
     if out is None:
         out = torch.empty(rows, d, dtype=torch.float32, device=patch_out.device)
     _t0 = _begin()
     _lib.check(_lib.lib.mmk_embed_tokens(patch_out.data_ptr(), _p(tile_image), _p(tile_slot), _p(image_ar),
-                                         total_tiles, patches_per_tile, d, cls.data_ptr(), pos.data_ptr(),
+                                         total_tiles, patches_per_tile, d, _p(cls), pos.data_ptr(),
                                          float(pos_scale), _p(tile_pos), float(tile_pos_scale), _p(pre_tile),
-                                         float(pre_scale), slots, gamma.data_ptr(), beta.data_ptr(), float(eps),
+                                         float(pre_scale), slots, _p(gamma), _p(beta), float(eps),
                                          out.data_ptr(), _s()))
     _end('embed', out.numel() * 8.0, _t0)
     return out

@@ -42,8 +42,9 @@ def init_weights(spec: ModelSpec, seed: int = 0, gate_scale: float = 0.5) -> dic
 
     W: dict = {}
     W["patch_w"] = _bf16_exact(nrm(d, 3 * enc.patch_px ** 2))
-    W["cls"] = nrm(d, s=d ** -0.5)
-    W["pos"] = nrm(P + 1, d, s=d ** -0.5)
+    W["patch_b"] = nrm(d) if enc.patch_bias else None
+    W["cls"] = nrm(d, s=d ** -0.5) if enc.cls_token else None
+    W["pos"] = nrm(P + int(enc.cls_token), d, s=d ** -0.5)
     for nm in ("pre_ln", "post_ln"):
         W[nm + "_w"] = 1.0 + nrm(d)
         W[nm + "_b"] = nrm(d)

@@ -127,7 +127,7 @@ def main():
         dev = torch.device("cuda", local)
         if args.handoff == "peer":
             enc = spec.encoder
-            P1 = (spec.tile_edge_px // enc.patch_px) ** 2 + 1
+            P1 = spec.seq_per_tile
             width = enc.hidden * (1 + len(enc.out_layers)) if enc.family == "mllama" else enc.hidden
             chan = PeerShardChannel(rank, world, dev, torch.bfloat16, slot_rows=args.slot_images * spec.max_tiles_per_image * P1,
                                     width=width, **kw)

@@ -94,6 +94,21 @@ def test_vit_b16_batch8():
     _run(spec, [(224, 224)] * 8, seed=2)
 
 
+def test_llava_ov_siglip_reduced_depth_anyres():
+    """LLaVA-OneVision's SigLIP tower (reference presets llava-ov-7b / -72b): 384-px tiles with a
+    thumbnail (up to 10 tiles), 27x27 patches from 378 of 384 pixels, no class token, no pre-LN,
+    head_dim 72 run as zero-padded 80-wide heads, FFN 4304 padded to 4352, gelu_tanh; every tile is
+    its own attention sequence."""
+    from paper_2502_00937_b200 import core
+    spec = _reduced(core.get_model_spec("llava-ov-7b"), layers=3)
+    _run(spec, [(384, 384), (1000, 700), (300, 2000), (800, 800)], seed=5)
+
+
+def test_llava_ov_siglip_full_depth():
+    from paper_2502_00937_b200 import core
+    _run(core.get_model_spec("llava-ov-7b"), [(700, 500), (384, 384)], seed=6)
+
+
 def test_clip_l336_full_depth():
     """Full 24-layer CLIP ViT-L/14-336 to layer -2 (LLaVA feature layer), CLS dropped."""
     from paper_2502_00937_b200 import core

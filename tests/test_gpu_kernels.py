@@ -113,7 +113,7 @@ def test_preprocess_mllama_bit_exact(mk):
     _check_preprocess(core, ops, encoders, spec, dims)
 
 
-@pytest.mark.parametrize("model", ["llama3.2-11b", "llava-clip-l14-336", "vit-b16-224"])
+@pytest.mark.parametrize("model", ["llama3.2-11b", "llava-clip-l14-336", "vit-b16-224", "llava-ov-7b"])
 def test_preprocess_generator_extremes_bit_exact(mk, model):
     """The generator's clip range (64..4096 px per side, workload.py:143-178): largest images,
     extreme aspect ratios in both orientations, and one-pixel strips."""

@@ -283,3 +283,45 @@ def test_mllama_ragged_oracle_equals_faithful_when_hf_pads_nothing():
         ragged = oenc.mllama_image(patches, W, spec.encoder, ar, n)
         faithful = oenc.mllama_image_hf(patches, W, spec.encoder, ar, n, n)
         torch.testing.assert_close(ragged, faithful, rtol=1e-4, atol=1e-4)
+
+
+@torch.no_grad()
+def test_siglip_vision_matches_hf():
+    """SigLIP (LLaVA-OneVision's vision tower): no class token, no pre-LN, conv bias, gelu_tanh,
+    384 / 14 -> a floor 27-patch grid; the feature LLaVA-OV takes (vision_feature_layer -1) is the
+    encoder output before post_layernorm."""
+    from types import SimpleNamespace
+
+    from transformers import SiglipVisionConfig, SiglipVisionModel
+    d, ff, heads, layers, T, p = 72, 136, 4, 3, 46, 14  # 46 / 14 -> 3x3 patches, 4 trailing pixels unused
+    cfg = SiglipVisionConfig(hidden_size=d, intermediate_size=ff, num_attention_heads=heads, num_hidden_layers=layers,
+                             image_size=T, patch_size=p, hidden_act="gelu_pytorch_tanh", layer_norm_eps=1e-6)
+    m = SiglipVisionModel(cfg).eval()
+    g = torch.Generator().manual_seed(9)
+    P = (T // p) ** 2
+    W = {"patch_w": 0.05 * torch.randn(d, 3 * p * p, generator=g), "patch_b": 0.1 * torch.randn(d, generator=g),
+         "pos": torch.randn(P, d, generator=g) * 0.1}
+    for i in range(layers):
+        _rand_block(W, f"l{i}.", d, ff, g)
+    vm = m.vision_model
+    vm.embeddings.patch_embedding.weight.data.copy_(W["patch_w"].view(d, 3, p, p))
+    vm.embeddings.patch_embedding.bias.data.copy_(W["patch_b"])
+    vm.embeddings.position_embedding.weight.data.copy_(W["pos"])
+    for i, layer in enumerate(vm.encoder.layers):
+        pre = f"l{i}."
+        _load_attn(layer.self_attn, W, pre, d, True)
+        layer.layer_norm1.weight.data.copy_(W[pre + "ln1_w"])
+        layer.layer_norm1.bias.data.copy_(W[pre + "ln1_b"])
+        layer.layer_norm2.weight.data.copy_(W[pre + "ln2_w"])
+        layer.layer_norm2.bias.data.copy_(W[pre + "ln2_b"])
+        layer.mlp.fc1.weight.data.copy_(W[pre + "fc1_w"])
+        layer.mlp.fc1.bias.data.copy_(W[pre + "fc1_b"])
+        layer.mlp.fc2.weight.data.copy_(W[pre + "fc2_w"])
+        layer.mlp.fc2.bias.data.copy_(W[pre + "fc2_b"])
+    px = torch.randn(1, 3, T, T, generator=g)
+    hf = vm.encoder(inputs_embeds=vm.embeddings(px)).last_hidden_state[0]
+    g2 = T // p * p
+    patches = px[0, :, :g2, :g2].unfold(1, p, p).unfold(2, p, p).permute(1, 2, 0, 3, 4).reshape(P, 3 * p * p)
+    enc = SimpleNamespace(norm_eps=1e-6, layers=layers, heads=heads, act="gelu_tanh", drop_cls=False, out_layer=-1,
+                          cls_token=False, pre_ln=False)
+    torch.testing.assert_close(oenc.clip_image(patches, W, enc), hf, rtol=1e-4, atol=1e-4)
