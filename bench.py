@@ -49,7 +49,10 @@ WORKLOADS = {
     "llava-clip-l14-336": dict(config="LLaVA-style CLIP ViT-L/14-336, layer -2, CLS dropped, ragged packing",
                                batch=256, generator=dict()),
     "vit-b16-224": dict(config="reference default: 224x224 single tile -> ViT-B/16", batch=8, fixed=(224, 224)),
-
+    "llava-ov-7b": dict(config="LLaVA-OneVision SigLIP-400M, 384px tiles (<=10) + thumbnail, bf16",
+                        batch=32, generator=dict()),
+    "internvl-26b": dict(config="InternVL-26B InternViT-6B, 448px tiles (<=5) + thumbnail, pixel shuffle, bf16",
+                         batch=32, generator=dict()),
 }
 
 
@@ -254,12 +257,19 @@ class MixSampler:
                 "same_config": True}
 
 
-def cpu_baseline_line(spec, dims, weights, seed, threads):
-    """One sample per tile count of the batch (~10-30 s of CPU work), weighted by the batch mix."""
+def cpu_baseline_line(spec, dims, weights, seed, threads, budget_s: float = 30.0):
+    """One sample per tile count of the batch, most frequent first, until ~``budget_s`` of CPU
+    work (InternViT-6B: ~10 s per tile); the batch time is weighted by the batch mix, tile counts
+    left unsampled scaled by encoder FLOPs."""
     ms = MixSampler(spec, dims, seed)
+    spent = 0.0
     for _ in range(len(ms.hist)):
+        if spent > budget_s:
+            break
         t, imgs = ms.next_sample()
-        ms.record(t, cpu_reference_time(spec, imgs, weights, threads))
+        dt = cpu_reference_time(spec, imgs, weights, threads)
+        ms.record(t, dt)
+        spent += dt
     total, est = ms.batch_seconds()
     return {"value": round(len(dims) / total, 4), "unit": "images/s", "cores": threads, "kind": "port",
             "sample": f"{ms.group} image(s) per tile count of the {len(dims)}-image batch, CPU time of the batch "
@@ -366,7 +376,7 @@ def main():
         try:
             import torch.distributed._symmetric_memory as symm
             enc = spec.encoder
-            width = enc.hidden * (1 + len(enc.out_layers)) if enc.family == "mllama" else enc.hidden
+            width = enc.out_width
             first = [sum(rank_rows[q] for q in range(r)) * width for r in range(world)]
             prefill = symm.empty(sum(rank_rows.values()) * width, dtype=torch.bfloat16, device="cuda")
             hdl = symm.rendezvous(prefill, dist.group.WORLD)
@@ -600,7 +610,8 @@ def main():
             "clocks": clk.result(),
         }
         if not args.no_cpu_baseline and world == 1:
-            line["cpu_baseline"] = cpu_baseline_line(spec, all_dims, ex.weights, 1000, len(os.sched_getaffinity(0)))
+            w_cpu = {k: (v.cpu() if isinstance(v, torch.Tensor) else v) for k, v in ex.weights.items()}
+            line["cpu_baseline"] = cpu_baseline_line(spec, all_dims, w_cpu, 1000, len(os.sched_getaffinity(0)))
         print(json.dumps(line), file=result_out, flush=True)
     if world > 1:
         dist.barrier()

@@ -122,11 +122,23 @@ int mmk_gemm_bf16_ln(const void* a, int64_t lda, const void* b, int64_t ldb, int
                      int32_t k, int32_t epilogue, const float* bias, void* out, int64_t ldo,
                      float gate, void* aux, int64_t ld_aux, float* ln_stats_out, const float* ln_mr,
                      const float* ln_c1, cudaStream_t stream);
-int mmk_ln_stats_finalize(const float* stats, int32_t rows, int32_t d, float eps, float* mr,
-                          cudaStream_t stream);
+int mmk_ln_stats_finalize(const float* stats, int32_t rows, int32_t d, float eps, int32_t rms, float* mr,
+                          cudaStream_t stream);  /* rms != 0: RMSNorm, mr = (0, 1/sqrt(mean(x^2) + eps)) */
+
+/* InternViT QK-norm: RMSNorm (weights q_w / k_w, f32 [d]) over each row's whole query columns
+ * [0, d) and key columns [d, 2d) of the bf16 [Q | K | V] matrix (row pitch ld), in place. */
+int mmk_qk_rmsnorm(void* qkv, int32_t rows, int32_t d, int64_t ld, const float* q_w, const float* k_w,
+                   float eps, cudaStream_t stream);
+
+/* InternVL pixel shuffle (downsample 0.5) into the prefill layout: each tile's side x side patch grid
+ * (fp32 rows, `drop` leading class tokens skipped) -> (side/2)^2 bf16 rows of 4 d columns,
+ * [f(2y,2x) | f(2y,2x+1) | f(2y+1,2x) | f(2y+1,2x+1)] (transformers InternVLModel.pixel_shuffle). */
+int mmk_pack_pixel_shuffle(const float* src, int32_t tiles, int32_t side, int32_t tokens_per_tile,
+                           int32_t drop, int32_t d, void* out, cudaStream_t stream);
 
 /*
- * K3 — row LayerNorm: y_bf16 = LN(x_f32) * gamma + beta (+ optional per-tile additive term).
+ * K3 — row LayerNorm: y_bf16 = LN(x_f32) * gamma + beta (+ optional per-tile additive term);
+ *   beta NULL: RMSNorm, y = x / sqrt(mean(x^2) + eps) * gamma (InternViT).
  *   x f32 [rows, d]; y bf16 [rows, d] (or f32 when y_f32 != 0, may alias x).
  *   tile_add (optional, f32 [n_tables, slots, d]) :
  *       y += tile_add[image_table[tile_image[tile]], tile_slot[tile]],  tile = row / rows_per_tile
@@ -137,11 +149,16 @@ int mmk_layernorm(const float* x, void* y, int32_t y_f32, int32_t rows, int32_t 
                   const int32_t* tile_image, const int32_t* image_table, const int32_t* tile_slot,
                   int32_t rows_per_tile, int32_t slots, cudaStream_t stream);
 
+/* Row LayerNorm of bf16 rows of any width (multiple of 8), bf16 out (may alias x): the InternVL
+ * projector's LayerNorm(4 d) over pixel-shuffled tokens on the LLM side. */
+int mmk_layernorm_bf16(const void* x, void* y, int32_t rows, int32_t d, const float* gamma, const float* beta,
+                       float eps, cudaStream_t stream);
+
 /*
  * K5 — non-causal variable-length multi-head self-attention (one sequence per image).
  *   qkv bf16 [T, 3*H*hd] = [Q | K | V] (head h at column h*hd inside each block)
  *   out bf16 [T, H*hd]; cu_seqlens int32 [n_seq+1] (device); total_tokens = T = cu_seqlens[n_seq]
- *   (host copy, bounds the TMA tensor maps); hd in {64, 80}; scale = hd^-0.5 typically.
+ *   (host copy, bounds the TMA tensor maps); hd in {64, 80, 128}; scale = hd^-0.5 typically.
  *   workspace: device memory of mmk_attention_workspace_size() bytes, overwritten (the persistent
  *   kernel's work-item counter, reset on `stream`); not to be shared by concurrent calls.
  */

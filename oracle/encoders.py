@@ -8,6 +8,11 @@ transformers 5.5 (in this image) — cross-checked against those modules in test
 * CLIP-style pre-LN ViT: models/clip/modeling_clip.py (embeddings :138-220, pre_layrnorm ->
   encoder -> post_layernorm :647-697), QuickGELU activations.py:117-123.  LLaVA takes
   hidden_states[-2] and drops the CLS token.
+* InternViT-6B (InternVL / NVLM presets): models/internvl/modeling_internvl.py — RMSNorm
+  (InternVLVisionRMSNorm), q_norm / k_norm over the whole projection, lambda_1 / lambda_2 layer
+  scale (InternVLVisionLayer), class token + absolute positions, no pre/post norm
+  (use_mean_pooling), then InternVLModel.get_image_features: drop the class token and
+  pixel_shuffle(0.5) the 32x32 grid (the multi_modal_projector is the LLM side's, not emitted).
 * Mllama vision: models/mllama/modeling_mllama.py:846-1039 — gated pre/post tile embeddings
   (:105-124), gated position + tile-position embedding (:127-162), 32 ungated + 8 gated layers
   (:274-314), intermediate hidden states [3,7,15,23,30] concatenated (stack(dim=-1) order).
@@ -28,6 +33,9 @@ import torch.nn.functional as Fn
 
 
 def _ln(x, w, b, eps):
+    """LayerNorm, or RMSNorm when there is no bias (InternVLVisionRMSNorm: x * rsqrt(mean(x^2) + eps) * w)."""
+    if b is None:
+        return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + eps) * w
     return Fn.layer_norm(x, (x.shape[-1],), w, b, eps)
 
 
@@ -44,11 +52,14 @@ def _layer(h, W, pre, heads, act, eps, gated=False, mask=None):
     additive [S, S] attention bias, used only by the HF-faithful Mllama mode)."""
     S, d = h.shape
     hd = d // heads
-    x = _ln(h, W[pre + "ln1_w"], W[pre + "ln1_b"], eps)
+    x = _ln(h, W[pre + "ln1_w"], W.get(pre + "ln1_b"), eps)
     qkv = x @ W[pre + "qkv_w"].t()
     if W.get(pre + "qkv_b") is not None:
         qkv = qkv + W[pre + "qkv_b"]
     q, k, v = qkv.split(d, dim=-1)
+    if pre + "q_norm" in W:  # InternViT QK-norm: RMSNorm over all heads of q, of k
+        q = _ln(q, W[pre + "q_norm"], None, eps)
+        k = _ln(k, W[pre + "k_norm"], None, eps)
     q = q.view(S, heads, hd).transpose(0, 1)
     k = k.view(S, heads, hd).transpose(0, 1)
     v = v.view(S, heads, hd).transpose(0, 1)
@@ -58,12 +69,24 @@ def _layer(h, W, pre, heads, act, eps, gated=False, mask=None):
         a = a + W[pre + "o_b"]
     if gated:
         a = math.tanh(float(W[pre + "gate_attn"])) * a
+    if pre + "ls1" in W:
+        a = W[pre + "ls1"] * a
     h = h + a
-    x = _ln(h, W[pre + "ln2_w"], W[pre + "ln2_b"], eps)
+    x = _ln(h, W[pre + "ln2_w"], W.get(pre + "ln2_b"), eps)
     m = _act(x @ W[pre + "fc1_w"].t() + W[pre + "fc1_b"], act) @ W[pre + "fc2_w"].t() + W[pre + "fc2_b"]
     if gated:
         m = math.tanh(float(W[pre + "gate_ffn"])) * m
+    if pre + "ls2" in W:
+        m = W[pre + "ls2"] * m
     return h + m
+
+
+def pixel_shuffle(x: torch.Tensor, side: int) -> torch.Tensor:
+    """[side*side, C] patch grid (row-major) -> [(side/2)^2, 4C]: InternVLModel.pixel_shuffle
+    (scale 0.5) restated — output token (y, x) = [f(2y,2x) | f(2y,2x+1) | f(2y+1,2x) | f(2y+1,2x+1)]."""
+    C = x.shape[1]
+    g = x.view(side // 2, 2, side // 2, 2, C)  # [y, i, x, j, C]
+    return g.permute(0, 2, 1, 3, 4).reshape((side // 2) ** 2, 4 * C)
 
 
 def patch_embed(patches: torch.Tensor, W) -> torch.Tensor:
@@ -74,7 +97,8 @@ def patch_embed(patches: torch.Tensor, W) -> torch.Tensor:
 
 
 def clip_image(patches: torch.Tensor, W, enc) -> torch.Tensor:
-    """One single-tile image: patches [P, k_pad] -> emitted tokens [P + cls - drop_cls, d].
+    """One single-tile image: patches [P, k_pad] -> emitted tokens [P + cls - drop_cls, d]
+    (pixel_shuffle: [P/4, 4d]).
     SigLIP (modeling_siglip.py: SiglipVisionEmbeddings, no class token, no pre-LN, conv bias,
     gelu_pytorch_tanh) is the same family with cls_token / pre_ln off."""
     eps = enc.norm_eps
@@ -87,7 +111,10 @@ def clip_image(patches: torch.Tensor, W, enc) -> torch.Tensor:
         h = _layer(h, W, f"l{i}.", enc.heads, enc.act, eps)
     # hidden_states[out_layer] of CLIPVisionModel: post_layernorm is applied to the pooled CLS
     # only (modeling_clip.py), never to the emitted sequence
-    return h[1:] if getattr(enc, "drop_cls", False) else h
+    h = h[1:] if getattr(enc, "drop_cls", False) else h
+    if getattr(enc, "pixel_shuffle", False):
+        h = pixel_shuffle(h, int(round(h.shape[0] ** 0.5)))
+    return h
 
 
 def mllama_image(patches: torch.Tensor, W, enc, ar_id: int, n_tiles: int) -> torch.Tensor:

@@ -37,7 +37,10 @@ SIGNATURES = {
     "mmk_gemm_bf16": ([_V, _I64, _V, _I64, _I32, _I32, _I32, _I32, _V, _V, _I64, _F, _V, _I64, _V], _I32),
     "mmk_gemm_bf16_ln": ([_V, _I64, _V, _I64, _I32, _I32, _I32, _I32, _V, _V, _I64, _F, _V, _I64, _V, _V, _V, _V],
                          _I32),
-    "mmk_ln_stats_finalize": ([_V, _I32, _I32, _F, _V, _V], _I32),
+    "mmk_ln_stats_finalize": ([_V, _I32, _I32, _F, _I32, _V, _V], _I32),
+    "mmk_layernorm_bf16": ([_V, _V, _I32, _I32, _V, _V, _F, _V], _I32),
+    "mmk_qk_rmsnorm": ([_V, _I32, _I32, _I64, _V, _V, _F, _V], _I32),
+    "mmk_pack_pixel_shuffle": ([_V, _I32, _I32, _I32, _I32, _I32, _V, _V], _I32),
     "mmk_layernorm": ([_V, _V, _I32, _I32, _I32, _V, _V, _F, _V, _V, _V, _V, _I32, _I32, _V], _I32),
     "mmk_attention_workspace_size": ([], _I64),
     "mmk_attention_varlen_bf16": ([_V, _V, _V, _I32, _I32, _I32, _I32, _I32, _F, _V, _V], _I32),

@@ -24,11 +24,13 @@ extern "C" int mmk_attention_varlen_bf16(const void* qkv, void* out, const int32
                                          float scale, void* workspace, cudaStream_t stream) {
   if (n_seq < 0 || heads <= 0 || max_seqlen < 0 || total_tokens < 0)
     return set_error(MMK_ERR_ARG, "attention: bad shape");
-  if (head_dim != 64 && head_dim != 80)
-    return set_error(MMK_ERR_UNSUPPORTED, "attention: head_dim %d not in {64, 80}", head_dim);
+  if (head_dim != 64 && head_dim != 80 && head_dim != 128)
+    return set_error(MMK_ERR_UNSUPPORTED, "attention: head_dim %d not in {64, 80, 128}", head_dim);
   if (n_seq == 0 || max_seqlen == 0 || total_tokens == 0) return MMK_OK;
   if (workspace == nullptr) return set_error(MMK_ERR_ARG, "attention: workspace is NULL");
   if (head_dim == 64)
     return launch_attn_tc<64>(qkv, out, cu_seqlens, n_seq, max_seqlen, heads, scale, total_tokens, workspace, stream);
+  if (head_dim == 128)
+    return launch_attn_tc<128>(qkv, out, cu_seqlens, n_seq, max_seqlen, heads, scale, total_tokens, workspace, stream);
   return launch_attn_tc<80>(qkv, out, cu_seqlens, n_seq, max_seqlen, heads, scale, total_tokens, workspace, stream);
 }

@@ -67,11 +67,14 @@ struct TcAttnCfg {
   static constexpr bool kLSum = MMK_ATTN_LSUM && HD == 80;   // l accumulated by the tensor core
   static constexpr int kOCols = HD + (kLSum ? 16 : 0);       // O_t columns (+ the l block)
   static constexpr bool kRem = (HD % 64) != 0;               // has a 16-wide remainder block
-  static constexpr int kQMain = kTcBQ * 64 * 2;              // Q tile: 128 rows x 64 cols
+  static constexpr int kBlocks = HD / 64;                    // 64-column main blocks (2 for hd 128)
+  static constexpr int kQBlock = kTcBQ * 64 * 2;             // one main block of Q: 128 rows x 64 cols
+  static constexpr int kQMain = kBlocks * kQBlock;
   static constexpr int kQBytes = kQMain + (kRem ? kTcBQ * 16 * 2 : 0);
-  static constexpr int kKVMain = BKV * 64 * 2;               // K or V tile: BKV rows x 64 cols
+  static constexpr int kKVBlock = BKV * 64 * 2;              // one main block of K or V: BKV rows x 64 cols
+  static constexpr int kKVMain = kBlocks * kKVBlock;
   static constexpr int kKVBytes = kKVMain + (kRem ? BKV * 16 * 2 : 0);
-  static constexpr int STAGES = 4;
+  static constexpr int STAGES = HD > 80 ? 2 : 4;             // hd 128: the persistent kernel's two Q slots fill smem
   static constexpr int kQOff = 0;
   static constexpr int kKVOff = NQ * kQBytes;
   static constexpr int kStageBytes = 2 * kKVBytes;           // K then V
@@ -148,10 +151,13 @@ template <int HD, int BKV, int NQ>
 MMK_DEV void issue_s(uint32_t s_tm, uint32_t q_addr, uint32_t k_addr) {
   using C = TcAttnCfg<HD, BKV, NQ>;
   constexpr uint32_t idesc_s = umma_idesc_bf16_f32(kTcBQ, BKV);
-  const uint64_t qd = umma_desc_sw128_kmajor(q_addr);
-  const uint64_t kd = umma_desc_sw128_kmajor(k_addr);
 #pragma unroll
-  for (int k = 0; k < 4; ++k) umma_bf16_ss(s_tm, qd + 2 * k, kd + 2 * k, idesc_s, k > 0);
+  for (int b = 0; b < C::kBlocks; ++b) {
+    const uint64_t qd = umma_desc_sw128_kmajor(q_addr + b * C::kQBlock);
+    const uint64_t kd = umma_desc_sw128_kmajor(k_addr + b * C::kKVBlock);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) umma_bf16_ss(s_tm, qd + 2 * k, kd + 2 * k, idesc_s, (b | k) > 0);
+  }
   if (C::kRem)
     umma_bf16_ss(s_tm, umma_desc_sw32_kmajor(q_addr + C::kQMain), umma_desc_sw32_kmajor(k_addr + C::kKVMain),
                  idesc_s, 1u);
@@ -173,13 +179,15 @@ MMK_DEV void issue_pv(uint32_t o_tm, uint32_t p_tm, uint32_t v_addr, bool first,
   constexpr uint32_t idesc_pv_main = umma_idesc_bf16_f32(kTcBQ, 64) | (1u << 16);  // B (V) MN-major
   constexpr uint32_t idesc_pv_rem = umma_idesc_bf16_f32(kTcBQ, 16) | (1u << 16);
   constexpr uint32_t kVStepMain = (16 * 128) >> 4, kVStepRem = (16 * 32) >> 4;  // desc units per k-step
-  const uint64_t vd_main = umma_desc_sw128_kmajor(v_addr);              // MN-major, SBO 1024
   const uint64_t vd_rem = umma_desc_sw32_kmajor(v_addr + C::kKVMain);  // MN-major, SBO 256
 #pragma unroll
   for (int k = 0; k < BKV / 16; ++k) {
     const uint32_t acc = (!first || k > 0) ? 1u : 0u;
-    umma_bf16_ts(o_tm, p_tm + 8 * k, vd_main + kVStepMain * k, idesc_pv_main, acc);
-    if (C::kRem) umma_bf16_ts(o_tm + 64, p_tm + 8 * k, vd_rem + kVStepRem * k, idesc_pv_rem, acc);
+#pragma unroll
+    for (int b = 0; b < C::kBlocks; ++b)  // V block b -> O columns [64 b, 64 b + 64); MN-major, SBO 1024
+      umma_bf16_ts(o_tm + 64 * b, p_tm + 8 * k, umma_desc_sw128_kmajor(v_addr + b * C::kKVBlock) + kVStepMain * k,
+                   idesc_pv_main, acc);
+    if (C::kRem) umma_bf16_ts(o_tm + 64 * C::kBlocks, p_tm + 8 * k, vd_rem + kVStepRem * k, idesc_pv_rem, acc);
     if constexpr (C::kLSum) umma_bf16_ts(o_tm + HD, p_tm + 8 * k, umma_desc_sw32_kmajor(ones_addr), idesc_pv_rem, acc);
   }
 }
@@ -566,8 +574,9 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
       mbar_arrive_expect_tx(q_full, n_qt * C::kQBytes);
       for (int t = 0; t < n_qt; ++t) {
         uint8_t* q = tile_ptr(C::kQOff + t * C::kQBytes);
-        tma_load_2d(&tm_q, q_full, q, col_q, s_begin + q0 + t * kTcBQ);
-        if (C::kRem) tma_load_2d(&tm_q_rem, q_full, q + C::kQMain, col_q + 64, s_begin + q0 + t * kTcBQ);
+        for (int b = 0; b < C::kBlocks; ++b)
+          tma_load_2d(&tm_q, q_full, q + b * C::kQBlock, col_q + 64 * b, s_begin + q0 + t * kTcBQ);
+        if (C::kRem) tma_load_2d(&tm_q_rem, q_full, q + C::kQMain, col_q + 64 * C::kBlocks, s_begin + q0 + t * kTcBQ);
       }
       for (int j = 0; j < nkv; ++j) {
         const int st = j % C::STAGES;
@@ -577,11 +586,11 @@ attn_fwd_tc(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CU
         uint8_t* vt = kt + C::kKVBytes;
         const int row = s_begin + j * BKV;
         mbar_arrive_expect_tx(&k_full[st], C::kKVBytes);
-        tma_load_2d(&tm_kv, &k_full[st], kt, col_k, row);
-        if (C::kRem) tma_load_2d(&tm_kv_rem, &k_full[st], kt + C::kKVMain, col_k + 64, row);
+        for (int b = 0; b < C::kBlocks; ++b) tma_load_2d(&tm_kv, &k_full[st], kt + b * C::kKVBlock, col_k + 64 * b, row);
+        if (C::kRem) tma_load_2d(&tm_kv_rem, &k_full[st], kt + C::kKVMain, col_k + 64 * C::kBlocks, row);
         mbar_arrive_expect_tx(&v_full[st], C::kKVBytes);
-        tma_load_2d(&tm_kv, &v_full[st], vt, col_v, row);
-        if (C::kRem) tma_load_2d(&tm_kv_rem, &v_full[st], vt + C::kKVMain, col_v + 64, row);
+        for (int b = 0; b < C::kBlocks; ++b) tma_load_2d(&tm_kv, &v_full[st], vt + b * C::kKVBlock, col_v + 64 * b, row);
+        if (C::kRem) tma_load_2d(&tm_kv_rem, &v_full[st], vt + C::kKVMain, col_v + 64 * C::kBlocks, row);
       }
     }
   } else if (warp > kTmaWarp) {
@@ -890,8 +899,8 @@ attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_co
         for (int t = 0; t < it.n_qt; ++t) {
           uint8_t* q = tile_ptr(Lay::kQOff + qs * Lay::kQSlotBytes + t * C::kQBytes);
           const int row = it.s_begin + it.q0 + t * kTcBQ;
-          tma_load_2d(&tm_q, &q_full[qs], q, col_q, row);
-          if (C::kRem) tma_load_2d(&tm_q_rem, &q_full[qs], q + C::kQMain, col_q + 64, row);
+          for (int b = 0; b < C::kBlocks; ++b) tma_load_2d(&tm_q, &q_full[qs], q + b * C::kQBlock, col_q + 64 * b, row);
+          if (C::kRem) tma_load_2d(&tm_q_rem, &q_full[qs], q + C::kQMain, col_q + 64 * C::kBlocks, row);
         }
         ++qi;
         for (int j = 0; j < it.nkv; ++j, ++kv) {
@@ -901,11 +910,11 @@ attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_co
           uint8_t* vt = kt + C::kKVBytes;
           const int row = it.s_begin + j * BKV;
           mbar_arrive_expect_tx(&k_full[st], C::kKVBytes);
-          tma_load_2d(&tm_kv, &k_full[st], kt, col_k, row);
-          if (C::kRem) tma_load_2d(&tm_kv_rem, &k_full[st], kt + C::kKVMain, col_k + 64, row);
+          for (int b = 0; b < C::kBlocks; ++b) tma_load_2d(&tm_kv, &k_full[st], kt + b * C::kKVBlock, col_k + 64 * b, row);
+          if (C::kRem) tma_load_2d(&tm_kv_rem, &k_full[st], kt + C::kKVMain, col_k + 64 * C::kBlocks, row);
           mbar_arrive_expect_tx(&v_full[st], C::kKVBytes);
-          tma_load_2d(&tm_kv, &v_full[st], vt, col_v, row);
-          if (C::kRem) tma_load_2d(&tm_kv_rem, &v_full[st], vt + C::kKVMain, col_v + 64, row);
+          for (int b = 0; b < C::kBlocks; ++b) tma_load_2d(&tm_kv, &v_full[st], vt + b * C::kKVBlock, col_v + 64 * b, row);
+          if (C::kRem) tma_load_2d(&tm_kv_rem, &v_full[st], vt + C::kKVMain, col_v + 64 * C::kBlocks, row);
         }
       }
     }
@@ -1115,7 +1124,9 @@ int launch_attn_tc(const void* qkv, void* out, const int32_t* cu, int n_seq, int
 #define MMK_ATTN_HD80_BKV 112
 #define MMK_ATTN_HD80_NQ 2
 #endif
-  constexpr int BKV = HD == 64 ? 64 : MMK_ATTN_HD80_BKV, NQ = HD == 64 ? 3 : MMK_ATTN_HD80_NQ;
+  // hd 128 (InternViT): 2 query tiles, 64-key tiles: S 2x64 + O 2x128 + P 2x32 = 448 columns
+  constexpr int BKV = HD == 64 ? 64 : HD == 128 ? 64 : MMK_ATTN_HD80_BKV;
+  constexpr int NQ = HD == 64 ? 3 : HD == 128 ? 2 : MMK_ATTN_HD80_NQ;
   const int64_t items = static_cast<int64_t>((max_s + NQ * kTcBQ - 1) / (NQ * kTcBQ)) * heads * n_seq;
   const bool persist = force == 1 || (force != 0 && items > 2 * num_sms());
   if (persist) {
@@ -1128,6 +1139,7 @@ int launch_attn_tc(const void* qkv, void* out, const int32_t* cu, int n_seq, int
 
 template int launch_attn_tc<64>(const void*, void*, const int32_t*, int, int, int, float, int64_t, void*, cudaStream_t);
 template int launch_attn_tc<80>(const void*, void*, const int32_t*, int, int, int, float, int64_t, void*, cudaStream_t);
+template int launch_attn_tc<128>(const void*, void*, const int32_t*, int, int, int, float, int64_t, void*, cudaStream_t);
 
 }  // namespace mmk
 

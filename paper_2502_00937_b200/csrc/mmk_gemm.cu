@@ -423,7 +423,9 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
   const uint32_t lane = lane_id();
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
-  const int n_tiles_n = N / BN;
+  // N % 64 == 0: the last N tile may be partial (InternViT d 3200, SigLIP 1152): B rows past N
+  // load as zeros (TMA out-of-bounds fill), stores past N are clipped by the output map or skipped
+  const int n_tiles_n = (N + BN - 1) / BN;
   const int n_tiles = ((M + 255) / 256) * n_tiles_n;
   const int num_kb = (K + kGemmBK - 1) / kGemmBK;
   const int first = static_cast<int>(cluster_id_x()), step = static_cast<int>(n_clusters_x());
@@ -559,6 +561,7 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(tempty_leader0 + acc * 8);
           }
+          if (n0 + col_in_tile >= N) continue;  // past a partial last N tile (no store, same buffer next)
           epilogue_bf16_tma<EPI>(r0, r1, n0 + col_in_tile, m0 + static_cast<int>(q) * 32, lane, bias,
                                  ebuf + sb * 4096, &tmap_out, lf.c1, mr);
           sb ^= 1;
@@ -585,10 +588,11 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
           const int slot = c & 1;
           mbar_wait(&res_bar[(warp - 4) * 2 + slot], (2 * t + (c >> 1)) & 1);  // two uses per slot per tile
           uint8_t* rowp = ebuf + slot * 4096 + lane * 128;
+          const bool col_ok = col < N;  // chunks past a partial last N tile: zeros in, store clipped
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-          if (bias != nullptr) {
+          if (bias != nullptr && col_ok) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
               const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + col + i));
@@ -606,11 +610,11 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
             *p4 = rr;
             v[4 * j] = rr.x; v[4 * j + 1] = rr.y; v[4 * j + 2] = rr.z; v[4 * j + 3] = rr.w;
           }
-          if (lf.stats_out != nullptr && row_ok)
+          if (lf.stats_out != nullptr && row_ok && col_ok)
             chunk_stats(v, lf.stats_out + static_cast<int64_t>(row) * (N / 32) + col / 32);
           fence_proxy_async();
           __syncwarp();
-          if (aux != nullptr) {
+          if (aux != nullptr && col_ok) {
             // bf16 copy of the updated 32x32 chunk, read back from the slot transposed so that a
             // warp store covers 8 whole 64-byte row segments (a row per lane would scatter each
             // store over 32 rows): lane = 4 r + cc writes columns 8cc..8cc+7 of row 8k + r
@@ -663,7 +667,7 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-          if (bias != nullptr) {
+          if (bias != nullptr && col < N) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
               const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + col + i));
@@ -692,7 +696,7 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
           uint32_t r[32];
           tmem_ld_32x32b_x32(tm_row + col_in_tile, r);
           tmem_ld_wait();
-          if (!row_ok) continue;
+          if (!row_ok || col >= N) continue;
           epilogue_chunk<EPI>(r, row, col, bias, out, ldo, gate, aux, ld_aux, lf,
                               lf.mr != nullptr ? lf.mr[row] : make_float2(0.f, 1.f), N);
         }
@@ -757,7 +761,7 @@ static int launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, const C
   static std::atomic<uint64_t> attr_done{0};  // per template instance
   if (int rc = ensure_smem_attr(reinterpret_cast<const void*>(kern), S::kTotal, attr_done, "gemm2: cudaFuncSetAttribute"))
     return rc;
-  const int tiles = ((M + 255) / 256) * (N / kGemm2BN);
+  const int tiles = ((M + 255) / 256) * ((N + kGemm2BN - 1) / kGemm2BN);
   const int pairs_max = num_sms() / 2;
   const int pairs = tiles < pairs_max ? tiles : pairs_max;
   cudaError_t e = launch_kernel(kern, dim3(2 * pairs), dim3(kGemmThreads), S::kTotal, stream, 2, tiles <= num_sms(), ta, tb, to, M, N, K,
@@ -812,11 +816,12 @@ extern "C" int mmk_gemm_bf16_ln(const void* a, int64_t lda, const void* b, int64
        reinterpret_cast<uintptr_t>(ln_stats_out)) & 15)
     return set_error(MMK_ERR_ARG, "gemm: LN pointers must be 16-byte aligned");
   const LnFold lf{reinterpret_cast<float2*>(ln_stats_out), reinterpret_cast<const float2*>(ln_mr), ln_c1};
-  // Kernel choice: CTA pairs (M=256 x N=256 tiles) when N splits into 256-wide tiles and there
-  // are enough tiles to occupy the pairs; otherwise the single-CTA kernel with BN 256 or 128.
+  // Kernel choice: CTA pairs (M=256 x N=256 tiles; N a multiple of 64, the last N tile possibly
+  // partial) when there are enough tiles to occupy the pairs; otherwise the single-CTA kernel
+  // with BN 256 or 128.
   static const bool no_2sm = getenv("MMK_GEMM_NO_2SM") != nullptr;  // A/B switch for profiling
-  const int tiles2 = ((m + 255) / 256) * (n / 256);
-  if (!no_2sm && n % 256 == 0 && tiles2 >= num_sms() / 2) {
+  const int tiles2 = ((m + 255) / 256) * ((n + 255) / 256);
+  if (!no_2sm && n % 64 == 0 && tiles2 >= num_sms() / 2) {
     CUtensorMap ta, tb;
     int rc = make_tmap_2d_bf16(&ta, a, k, m, lda, kGemmBK, 128, true);
     if (rc) return rc;

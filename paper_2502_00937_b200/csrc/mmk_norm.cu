@@ -42,6 +42,23 @@ MMK_DEV void ln_inplace(float4 (&x)[VEC], int d, const float* __restrict__ gamma
   }
 }
 
+// RMSNorm of the VEC float4 of this lane in place: x * rsqrt(mean(x^2) + eps) * gamma (InternViT).
+template <int VEC>
+MMK_DEV void rms_inplace(float4 (&x)[VEC], int d, const float* __restrict__ gamma, float eps, int lane) {
+  float q = 0.f;
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) q += (x[j].x * x[j].x + x[j].y * x[j].y) + (x[j].z * x[j].z + x[j].w * x[j].w);
+  const float rstd = rsqrtf(warp_sum(q) / d + eps);
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) {
+    const float4 g = __ldg(reinterpret_cast<const float4*>(gamma + lane * 4 + j * 128));
+    x[j].x = x[j].x * rstd * g.x;
+    x[j].y = x[j].y * rstd * g.y;
+    x[j].z = x[j].z * rstd * g.z;
+    x[j].w = x[j].w * rstd * g.w;
+  }
+}
+
 template <int VEC>
 MMK_DEV void store_row(void* y, int y_f32, int64_t row, int d, const float4 (&x)[VEC], int lane) {
 #pragma unroll
@@ -72,7 +89,8 @@ layernorm_kernel(const float* __restrict__ x, void* y, int y_f32, int rows, int 
   float4 v[VEC];
 #pragma unroll
   for (int j = 0; j < VEC; ++j) v[j] = *reinterpret_cast<const float4*>(x + row * d + lane * 4 + j * 128);
-  ln_inplace<VEC>(v, d, gamma, beta, eps, lane);
+  if (beta != nullptr) ln_inplace<VEC>(v, d, gamma, beta, eps, lane);
+  else rms_inplace<VEC>(v, d, gamma, eps, lane);  // no beta: RMSNorm
   if (tile_add != nullptr) {
     const int64_t tile = row / rows_per_tile;
     const float* add = tile_add + (static_cast<int64_t>(image_table[tile_image[tile]]) * slots + tile_slot[tile]) * d;
@@ -295,30 +313,180 @@ __global__ void checksum_kernel(const __nv_bfloat16* __restrict__ x, int64_t n, 
 static int grid_rows(int64_t rows) { return static_cast<int>((rows + 7) / 8); }
 
 // Folded LayerNorm: the producer GEMM's per-32-column (mean, M2) of a row -> (mu, rstd), merged
-// with Chan's formula (equal chunk counts); a thread per row.
+// with Chan's formula.  A warp per row: the lanes read the row's chunk statistics coalesced (up to
+// 2 chunks per lane, merged in registers), then a shuffle tree merges the lanes.
+MMK_DEV void chan_merge(float& n, float& mean, float& m2, float nb, float meanb, float m2b) {
+  const float nn = n + nb;
+  if (nb == 0.f) return;
+  if (n == 0.f) { n = nb; mean = meanb; m2 = m2b; return; }
+  const float delta = meanb - mean;
+  const float f = nb / nn;
+  mean = fmaf(delta, f, mean);
+  m2 = m2 + m2b + delta * delta * n * f;
+  n = nn;
+}
+
 __global__ void ln_stats_finalize_kernel(const float2* __restrict__ stats, int rows, int parts, float inv_d, float eps,
-                                         float2* __restrict__ mr) {
+                                         int rms, float2* __restrict__ mr) {
   griddep_wait();  // PDL: the statistics come from the preceding GEMM
   griddep_launch_dependents();
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= rows) return;
-  const float2* s = stats + static_cast<int64_t>(row) * parts;
-  float2 a = s[0];
-  float n = 32.f;
-  for (int i = 1; i < parts; ++i) {
+  const float2* s = stats + row * parts;
+  float n = 0.f, mean = 0.f, m2 = 0.f;
+  for (int i = lane; i < parts; i += 32) {
     const float2 b = s[i];
-    const float nn = n + 32.f;
-    const float delta = b.x - a.x;
-    a.x = fmaf(delta, 32.f / nn, a.x);
-    a.y = a.y + b.y + delta * delta * (n * 32.f / nn);
-    n = nn;
+    chan_merge(n, mean, m2, 32.f, b.x, b.y);
   }
-  mr[row] = make_float2(a.x, rsqrtf(fmaf(a.y, inv_d, eps)));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float nb = __shfl_xor_sync(0xffffffffu, n, o), mb = __shfl_xor_sync(0xffffffffu, mean, o),
+                m2b = __shfl_xor_sync(0xffffffffu, m2, o);
+    chan_merge(n, mean, m2, nb, mb, m2b);
+  }
+  if (lane == 0) {
+    if (rms)  // RMSNorm: no centring, mean(x^2) = M2 / n + mean^2
+      mr[row] = make_float2(0.f, rsqrtf(fmaf(m2, inv_d, fmaf(mean, mean, eps))));
+    else
+      mr[row] = make_float2(mean, rsqrtf(fmaf(m2, inv_d, eps)));
+  }
+}
+
+// QK-norm (InternViT use_qk_norm): RMSNorm over the whole query and the whole key projection of a
+// token (all heads, d columns each), in place on the bf16 [Q | K | V] rows; a warp per (row, Q or K).
+__global__ void __launch_bounds__(256)
+qk_rmsnorm_kernel(__nv_bfloat16* __restrict__ qkv, int rows, int d, int64_t ld, const float* __restrict__ q_w,
+                  const float* __restrict__ k_w, float eps) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const int lane = threadIdx.x & 31;
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (item >= 2ll * rows) return;
+  const int64_t row = item >> 1;
+  const int which = static_cast<int>(item & 1);  // 0: Q, 1: K
+  __nv_bfloat16* p = qkv + row * ld + which * d;
+  const float* w = which ? k_w : q_w;
+  float q = 0.f;
+  for (int c = lane * 8; c < d; c += 256) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p + c);
+    const uint32_t wv[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[i]));
+      q = fmaf(f.x, f.x, fmaf(f.y, f.y, q));
+    }
+  }
+  const float rstd = rsqrtf(warp_sum(q) / d + eps);
+  for (int c = lane * 8; c < d; c += 256) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p + c);
+    uint32_t wv[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[i]));
+      wv[i] = pack_bf16x2(f.x * rstd * __ldg(w + c + 2 * i), f.y * rstd * __ldg(w + c + 2 * i + 1));
+    }
+    *reinterpret_cast<uint4*>(p + c) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+  }
+}
+
+// InternVL pixel shuffle (downsample 0.5) of each tile's patch grid, CLS dropped: output token
+// (yj, xk) of a tile = [f(2yj, 2xk) | f(2yj, 2xk+1) | f(2yj+1, 2xk) | f(2yj+1, 2xk+1)] (4 d columns;
+// transformers InternVLModel.pixel_shuffle order).  A thread per (output row, 8 columns).
+__global__ void __launch_bounds__(256)
+pack_pixel_shuffle_kernel(const float* __restrict__ src, int64_t out_rows, int side, int tokens_per_tile, int drop,
+                          int d, __nv_bfloat16* __restrict__ out) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const int groups = 4 * d / 8;
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= out_rows * groups) return;
+  const int64_t orow = idx / groups;
+  const int c8 = static_cast<int>(idx - orow * groups) * 8;
+  const int half = side / 2;
+  const int64_t tile = orow / (half * half);
+  const int t = static_cast<int>(orow - tile * half * half);
+  const int yj = t / half, xk = t - yj * half;
+  const int q = c8 / d, c = c8 - q * d;
+  const int y = 2 * yj + (q >> 1), x = 2 * xk + (q & 1);
+  const float* s = src + (tile * tokens_per_tile + drop + y * side + x) * static_cast<int64_t>(d) + c;
+  const float4 a = *reinterpret_cast<const float4*>(s), b = *reinterpret_cast<const float4*>(s + 4);
+  st_global_v4(out + orow * (4ll * d) + c8, pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y),
+               pack_bf16x2(b.z, b.w));
+}
+
+// Wide-row LayerNorm on bf16 rows (the InternVL projector's LayerNorm(4 d) over pixel-shuffled
+// tokens, 12800 columns): a CTA per row; the row (<= 32 KB) is read from L1/L2 three times.
+__global__ void __launch_bounds__(256)
+layernorm_bf16_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y, int d,
+                      const float* __restrict__ gamma, const float* __restrict__ beta, float eps) {
+  griddep_wait();
+  griddep_launch_dependents();
+  __shared__ float red[8];
+  const int64_t row = blockIdx.x;
+  const __nv_bfloat16* xr = x + row * d;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto block_sum = [&](float v) {
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += red[i];
+    return t;
+  };
+  float s = 0.f;
+  for (int c = threadIdx.x * 8; c < d; c += 2048) {
+    const uint4 u = *reinterpret_cast<const uint4*>(xr + c);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+      s += f.x + f.y;
+    }
+  }
+  const float mean = block_sum(s) / d;
+  float q = 0.f;
+  for (int c = threadIdx.x * 8; c < d; c += 2048) {
+    const uint4 u = *reinterpret_cast<const uint4*>(xr + c);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+      q = fmaf(f.x - mean, f.x - mean, fmaf(f.y - mean, f.y - mean, q));
+    }
+  }
+  const float rstd = rsqrtf(block_sum(q) / d + eps);
+  for (int c = threadIdx.x * 8; c < d; c += 2048) {
+    const uint4 u = *reinterpret_cast<const uint4*>(xr + c);
+    uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+      const int k = c + 2 * i;
+      w[i] = pack_bf16x2(fmaf((f.x - mean) * rstd, __ldg(gamma + k), __ldg(beta + k)),
+                         fmaf((f.y - mean) * rstd, __ldg(gamma + k + 1), __ldg(beta + k + 1)));
+    }
+    *reinterpret_cast<uint4*>(y + row * d + c) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
 }
 
 }  // namespace mmk
 
 using namespace mmk;
+
+extern "C" int mmk_layernorm_bf16(const void* x, void* y, int32_t rows, int32_t d, const float* gamma,
+                                  const float* beta, float eps, cudaStream_t stream) {
+  if (rows < 0 || d <= 0 || d % 8 != 0 || gamma == nullptr || beta == nullptr)
+    return set_error(MMK_ERR_ARG, "layernorm_bf16: rows >= 0, d a multiple of 8, gamma and beta required");
+  if (rows == 0) return MMK_OK;
+  (void)launch_kernel(layernorm_bf16_kernel, dim3(static_cast<unsigned>(rows)), dim3(256), 0, stream, 1,
+                      rows <= kSmallRows, reinterpret_cast<const __nv_bfloat16*>(x),
+                      reinterpret_cast<__nv_bfloat16*>(y), d, gamma, beta, eps);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "layernorm_bf16: launch");
+}
 
 #define MMK_LN_CASE(V)                                                                                       \
   case V:                                                                                                    \
@@ -343,6 +511,7 @@ extern "C" int mmk_layernorm(const float* x, void* y, int32_t y_f32, int32_t row
     MMK_LN_CASE(10)
     MMK_LN_CASE(12)
     MMK_LN_CASE(16)
+    MMK_LN_CASE(25)
     default: return set_error(MMK_ERR_UNSUPPORTED, "layernorm: d=%d unsupported", d);
   }
   cudaError_t e = cudaGetLastError();
@@ -376,6 +545,7 @@ extern "C" int mmk_embed_tokens(const float* patch_out, const int32_t* tile_imag
     MMK_EMB_CASE(10)
     MMK_EMB_CASE(12)
     MMK_EMB_CASE(16)
+    MMK_EMB_CASE(25)
     default: return set_error(MMK_ERR_UNSUPPORTED, "embed: d=%d unsupported", d);
   }
   cudaError_t e = cudaGetLastError();
@@ -455,13 +625,38 @@ extern "C" int mmk_checksum_bf16(const void* x, int64_t n, float* out, cudaStrea
   return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "checksum: launch");
 }
 
-extern "C" int mmk_ln_stats_finalize(const float* stats, int32_t rows, int32_t d, float eps, float* mr,
+extern "C" int mmk_ln_stats_finalize(const float* stats, int32_t rows, int32_t d, float eps, int32_t rms, float* mr,
                                      cudaStream_t stream) {
   if (rows < 0 || d < 32 || d % 32 != 0) return set_error(MMK_ERR_ARG, "ln_stats_finalize: rows < 0 or d %% 32 != 0");
   if (rows == 0) return MMK_OK;
-  (void)launch_kernel(ln_stats_finalize_kernel, dim3((rows + 255) / 256), dim3(256), 0, stream, 1, rows <= kSmallRows,
-                      reinterpret_cast<const float2*>(stats), rows, d / 32, 1.f / static_cast<float>(d), eps,
+  (void)launch_kernel(ln_stats_finalize_kernel, dim3((rows + 7) / 8), dim3(256), 0, stream, 1, rows <= kSmallRows,
+                      reinterpret_cast<const float2*>(stats), rows, d / 32, 1.f / static_cast<float>(d), eps, rms,
                       reinterpret_cast<float2*>(mr));
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "ln_stats_finalize: launch");
+}
+
+extern "C" int mmk_qk_rmsnorm(void* qkv, int32_t rows, int32_t d, int64_t ld, const float* q_w, const float* k_w,
+                              float eps, cudaStream_t stream) {
+  if (rows < 0 || d <= 0 || d % 8 != 0 || ld < 3ll * d || ld % 8 != 0)
+    return set_error(MMK_ERR_ARG, "qk_rmsnorm: bad shape (d multiple of 8, ld >= 3 d)");
+  if (rows == 0) return MMK_OK;
+  (void)launch_kernel(qk_rmsnorm_kernel, dim3(grid_rows(2ll * rows)), dim3(256), 0, stream, 1, rows <= kSmallRows,
+                      reinterpret_cast<__nv_bfloat16*>(qkv), rows, d, static_cast<int64_t>(ld), q_w, k_w, eps);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "qk_rmsnorm: launch");
+}
+
+extern "C" int mmk_pack_pixel_shuffle(const float* src, int32_t tiles, int32_t side, int32_t tokens_per_tile,
+                                      int32_t drop, int32_t d, void* out, cudaStream_t stream) {
+  if (tiles < 0 || side < 2 || side % 2 || tokens_per_tile != side * side + drop || d % 8 != 0)
+    return set_error(MMK_ERR_ARG, "pack_pixel_shuffle: bad shape");
+  const int64_t out_rows = static_cast<int64_t>(tiles) * (side / 2) * (side / 2);
+  if (out_rows == 0) return MMK_OK;
+  const int64_t items = out_rows * (4ll * d / 8);
+  (void)launch_kernel(pack_pixel_shuffle_kernel, dim3(static_cast<unsigned>((items + 255) / 256)), dim3(256), 0, stream,
+                      1, out_rows <= kSmallRows, src, out_rows, side, tokens_per_tile, drop, d,
+                      reinterpret_cast<__nv_bfloat16*>(out));
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? MMK_OK : set_cuda_error(e, "pack_pixel_shuffle: launch");
 }

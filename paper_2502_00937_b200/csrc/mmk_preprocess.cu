@@ -32,7 +32,13 @@ namespace mmk {
 
 constexpr int kMaxPatch = 64;          // patch edge limit
 constexpr int kMaxSlots = 2 * kMaxPatch;
-constexpr int kStageBytes = 24 * 1024;  // staged source rows per chunk (3 CTAs/SM with a 47 KB band)
+#ifndef MMK_PREP_STAGE_KB
+#define MMK_PREP_STAGE_KB 24
+#endif
+#ifndef MMK_PREP_MAX_COLS
+#define MMK_PREP_MAX_COLS 1024  // output columns per CTA (two per thread)
+#endif
+constexpr int kStageBytes = MMK_PREP_STAGE_KB * 1024;  // staged source rows per chunk (3 CTAs/SM with a 47 KB band)
 constexpr int kPrepMaxThreads = 512;
 
 struct PrepImage {
@@ -407,7 +413,7 @@ extern "C" int mmk_preprocess(const uint8_t* src, const int64_t* src_off, int32_
   if (n == 0 || total_tiles == 0) return MMK_OK;
   const int per_side = tile_px / patch_px;
   int parts = 1;  // column parts per band: two columns per thread, at most kPrepMaxThreads threads
-  while ((per_side + parts - 1) / parts * patch_px > 2 * kPrepMaxThreads) ++parts;
+  while ((per_side + parts - 1) / parts * patch_px > MMK_PREP_MAX_COLS) ++parts;
   const int pc_per = (per_side + parts - 1) / parts;
   const int threads = (pc_per * patch_px / 2 + 31) / 32 * 32;
   const int band_bytes = (pc_per * k_pad * 2 + 127) & ~127;

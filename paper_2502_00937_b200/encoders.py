@@ -8,7 +8,9 @@ pkg/src/lmmsim/profiles.py:136-145, called from engine.py:693-703) with the real
   K8 FC2 GEMM + (gated) residual (+ intermediate capture) ] -> K9 pack
 
 Families (EncoderSpec.family):
-* "clip"   pre-LN ViT (ViT-B/16-224, CLIP ViT-L/14-336 as used by LLaVA: layer -2, no CLS)
+* "clip"   pre-LN ViT (ViT-B/16-224, CLIP ViT-L/14-336 as used by LLaVA: layer -2, no CLS;
+           SigLIP-400M of LLaVA-OneVision; InternViT-6B of InternVL / NVLM: RMSNorm, QK-norm,
+           layer scale folded into the O-proj / FC2 weights, pixel-shuffled output)
 * "mllama" Llama-3.2-Vision encoder: gated tile embeddings, 32 local + 8 gated global layers,
            output = [final | interleaved hidden_states[3,7,15,23,30]] (7680 wide;
            EncoderSpec.out_layers_of fixes which hidden state index i names)
@@ -30,6 +32,13 @@ from .core import ModelSpec, SpecError
 from .weights import K_ALIGN, init_weights, k_pad_of  # noqa: F401  (re-exported)
 
 
+# Narrow encoders (ViT-B, d 768: its reference-default batch 8 is a launch-latency-bound 1 ms
+# step) keep the LN kernels: the fold saves HBM traffic such steps do not spend (measured -2 %).
+# The choice is per encoder, never per batch, so an image's embedding does not depend on which
+# batch it was encoded in (replay.py --verify re-encodes shards alone and compares bit for bit).
+FOLD_MIN_HIDDEN = 1024
+
+
 class DeviceEncoder:
     """Device-resident weights + the forward of one encoder over a ragged batch of tiles."""
 
@@ -37,7 +46,7 @@ class DeviceEncoder:
         enc = spec.encoder
         if enc is None:
             raise SpecError(f"{spec.name}: no encoder block")
-        if enc.head_dim > 80:
+        if enc.head_dim > 128:
             from ._lib import ProfileError
             raise ProfileError(f"{spec.name}: head_dim {enc.head_dim} not supported by the attention kernel")
         self.spec, self.enc, self.device = spec, enc, torch.device(device)
@@ -45,12 +54,15 @@ class DeviceEncoder:
         # zero Q/K columns leave the scores unchanged (scale stays head_dim^-0.5), zero V columns
         # give zero output columns, which meet zero columns of the O-projection
         self.hd = enc.head_dim
-        self.hd_pad = 64 if enc.head_dim <= 64 else 80
+        self.hd_pad = 64 if enc.head_dim <= 64 else 80 if enc.head_dim <= 80 else 128
         # FFN widths that are not a multiple of 256 (SigLIP 4304) pad with zero units (act(0) = 0)
         self.ffn_pad = -(-enc.ffn // 256) * 256 if enc.ffn % 256 else enc.ffn
         # LayerNorm folded into the GEMMs (mmk_gemm_bf16_ln): every LN whose input comes from a
-        # residual GEMM; MMK_LN_FOLD=0 runs the separate LayerNorm kernel instead (A/B runs)
-        self.fold_ln = (os.environ.get("MMK_LN_FOLD", "1") != "0") if fold_ln is None else fold_ln
+        # residual GEMM; MMK_LN_FOLD=0 / =1 forces the separate LayerNorm kernel / the fold (A/B runs)
+        if fold_ln is None:
+            env = os.environ.get("MMK_LN_FOLD")
+            fold_ln = enc.hidden >= FOLD_MIN_HIDDEN if env is None else env != "0"
+        self.fold_ln = bool(fold_ln) and enc.hidden % 32 == 0
         self.P = (spec.tile_edge_px // enc.patch_px) ** 2
         self.S = self.P + int(enc.cls_token)  # encoder tokens per tile
         self.k_pad = k_pad_of(spec)
@@ -64,15 +76,29 @@ class DeviceEncoder:
         self.patch_b = f32(weights.get("patch_b"))
         self.cls, self.pos = f32(weights.get("cls")), f32(weights["pos"])
         self.pre_ln = (f32(weights["pre_ln_w"]), f32(weights["pre_ln_b"])) if enc.pre_ln else (None, None)
-        self.post_ln = (f32(weights["post_ln_w"]), f32(weights["post_ln_b"]))
+        self.post_ln = (f32(weights["post_ln_w"]), f32(weights.get("post_ln_b")))
+        self.rms = enc.norm == "rms"
+        if enc.qk_norm and enc.head_dim not in (64, 80, 128):
+            raise SpecError(f"{spec.name}: QK-norm with padded heads (head_dim {enc.head_dim}) is not supported")
 
         def folded(w, g, b, bias):
             """(W * gamma in bf16, c1 = row sums of it, c2 = beta W^T + bias): a LayerNorm with
-            (gamma, beta) in front of the GEMM W folded into the GEMM (see mmk_gemm_bf16_ln)."""
+            (gamma, beta) in front of the GEMM W folded into the GEMM (see mmk_gemm_bf16_ln); an
+            RMSNorm (beta None) has mean 0 in the epilogue, so c1 is unused and c2 = bias."""
             wf = (w.double() * g.double()[None, :]).to(torch.bfloat16)
             c1 = wf.double().sum(1)
-            c2 = w.double() @ b.double() + (bias.double() if bias is not None else 0.0)
+            c2 = torch.zeros(w.shape[0], dtype=torch.float64, device=w.device)
+            if b is not None:
+                c2 = c2 + w.double() @ b.double()
+            if bias is not None:
+                c2 = c2 + bias.double()
             return bf(wf), f32(c1.float()), f32(c2.float())
+
+        def scaled(w, b, ls):
+            """Layer scale lambda (per output channel) folded into the branch's last GEMM."""
+            if ls is None:
+                return w, b
+            return ls[:, None] * w, (ls * b if b is not None else None)
 
         H, hd, hdp, ff, ffp = enc.heads, self.hd, self.hd_pad, enc.ffn, self.ffn_pad
 
@@ -108,19 +134,22 @@ class DeviceEncoder:
         def block(pre, gated):
             qkv_w, qkv_b = pad_heads_rows(weights[pre + "qkv_w"]), pad_heads_rows(weights.get(pre + "qkv_b"))
             fc1_w, fc1_b = pad_ffn_rows(weights[pre + "fc1_w"]), pad_ffn_rows(weights[pre + "fc1_b"])
+            o_w, o_b = scaled(pad_heads_cols(weights[pre + "o_w"]), weights.get(pre + "o_b"), weights.get(pre + "ls1"))
+            fc2_w, fc2_b = scaled(pad_ffn_cols(weights[pre + "fc2_w"]), weights[pre + "fc2_b"], weights.get(pre + "ls2"))
             L = {
-                "ln1": (f32(weights[pre + "ln1_w"]), f32(weights[pre + "ln1_b"])),
+                "ln1": (f32(weights[pre + "ln1_w"]), f32(weights.get(pre + "ln1_b"))),
                 "qkv_w": bf(qkv_w), "qkv_b": f32(qkv_b),
-                "o_w": bf(pad_heads_cols(weights[pre + "o_w"])), "o_b": f32(weights.get(pre + "o_b")),
-                "ln2": (f32(weights[pre + "ln2_w"]), f32(weights[pre + "ln2_b"])),
+                "o_w": bf(o_w), "o_b": f32(o_b),
+                "ln2": (f32(weights[pre + "ln2_w"]), f32(weights.get(pre + "ln2_b"))),
                 "fc1_w": bf(fc1_w), "fc1_b": f32(fc1_b),
-                "fc2_w": bf(pad_ffn_cols(weights[pre + "fc2_w"])), "fc2_b": f32(weights[pre + "fc2_b"]),
+                "fc2_w": bf(fc2_w), "fc2_b": f32(fc2_b),
                 "gate_attn": math.tanh(float(weights[pre + "gate_attn"])) if gated else 1.0,
                 "gate_ffn": math.tanh(float(weights[pre + "gate_ffn"])) if gated else 1.0,
+                "qk_norm": (f32(weights[pre + "q_norm"]), f32(weights[pre + "k_norm"])) if enc.qk_norm else None,
             }
             if self.fold_ln:
-                L["qkv_f"] = folded(qkv_w, weights[pre + "ln1_w"], weights[pre + "ln1_b"], qkv_b)
-                L["fc1_f"] = folded(fc1_w, weights[pre + "ln2_w"], weights[pre + "ln2_b"], fc1_b)
+                L["qkv_f"] = folded(qkv_w, weights[pre + "ln1_w"], weights.get(pre + "ln1_b"), qkv_b)
+                L["fc1_f"] = folded(fc1_w, weights[pre + "ln2_w"], weights.get(pre + "ln2_b"), fc1_b)
             return L
 
         self.layers = [block(f"l{i}.", False) for i in range(enc.layers)]
@@ -154,6 +183,8 @@ class DeviceEncoder:
         else:
             ops.layernorm(resid, *L["ln1"], enc.norm_eps, out=x_buf)
             ops.gemm(x_buf, L["qkv_w"], ops.EPI_BF16, bias=L["qkv_b"], out=qkv_buf)
+        if L["qk_norm"] is not None:
+            ops.qk_rmsnorm(qkv_buf, enc.heads * self.hd_pad, *L["qk_norm"], enc.norm_eps)
         a_buf = x_buf if a_buf is None else a_buf  # attention output (H * padded head_dim columns)
         ops.attention(qkv_buf, cu, n_seq, max_s, enc.heads, self.hd_pad, out=a_buf, scale=self.hd ** -0.5,
                       sum_sq_seqlen=sum_sq * self.hd / self.hd_pad)
@@ -163,7 +194,7 @@ class DeviceEncoder:
             xr2 = qkv_buf[:, :d]
             ops.gemm(a_buf, L["o_w"], ops.EPI_RESID_F32, bias=L["o_b"], out=resid, gate=L["gate_attn"], aux=xr2,
                      ln_stats_out=ln[0])
-            ops.ln_stats_finalize(ln[0], T, d, enc.norm_eps, out=ln[1])
+            ops.ln_stats_finalize(ln[0], T, d, enc.norm_eps, out=ln[1], rms=self.rms)
             wf, c1, c2 = L["fc1_f"]
             ops.gemm(xr2, wf, ops.ACT_EPI[enc.act], bias=c2, out=h_buf, ln_mr=ln[1], ln_c1=c1)
         else:
@@ -176,7 +207,7 @@ class DeviceEncoder:
             dst = aux if aux is not None else x_buf
             ops.gemm(h_buf, L["fc2_w"], ops.EPI_RESID_F32, bias=L["fc2_b"], out=resid, gate=L["gate_ffn"], aux=dst,
                      ln_stats_out=ln[0])
-            ops.ln_stats_finalize(ln[0], T, d, enc.norm_eps, out=ln[1])
+            ops.ln_stats_finalize(ln[0], T, d, enc.norm_eps, out=ln[1], rms=self.rms)
             return dst
         ops.gemm(h_buf, L["fc2_w"], ops.EPI_RESID_F32, bias=L["fc2_b"], out=resid, gate=L["gate_ffn"], aux=aux)
         return None
@@ -188,9 +219,7 @@ class DeviceEncoder:
         if self.enc.heads * self.hd_pad != d:  # padded heads: the attention output is wider than d
             a_buf = torch.empty(T, self.enc.heads * self.hd_pad, dtype=torch.bfloat16, device=resid.device)
         ln = None
-        # small batches (ViT-B batch 8: 1576 rows, a launch-latency-bound step) keep the LN kernels:
-        # the fold's savings are HBM traffic, which such steps do not spend (measured -2 % there)
-        if self.fold_ln and d % 32 == 0 and T >= 16384:
+        if self.fold_ln:
             ln = (torch.empty(T, d // 32, 2, dtype=torch.float32, device=resid.device),
                   torch.empty(T, 2, dtype=torch.float32, device=resid.device))
         xr = None
@@ -226,6 +255,10 @@ class DeviceEncoder:
             # emitted = hidden_states[out_layer] as transformers' CLIPVisionModel numbers them
             # (modeling_clip.py: post_layernorm touches only the pooled CLS, never the sequence)
             drop = 1 if enc.drop_cls else 0
+            if enc.pixel_shuffle:  # InternVL: CLS dropped, 2x2 patch groups -> 4 d channels
+                side = self.spec.tile_edge_px // enc.patch_px
+                dst = out_alloc(total_tiles * (side // 2) ** 2, 4 * d) if out_alloc is not None else None
+                return ops.pack_pixel_shuffle(resid, total_tiles, side, S, drop, out=dst)
             dst = out_alloc(total_tiles * (S - drop), d) if out_alloc is not None else None
             return ops.pack_drop_cls(resid, total_tiles, S, drop, out=dst)
         # ---------------- mllama

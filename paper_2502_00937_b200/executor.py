@@ -23,6 +23,7 @@ from . import ops
 from .batcher import WorkItem
 from .core import ModelSpec, SpecError, StageKind, tile_count
 from .encoders import DeviceEncoder, init_weights
+from .weights import DEVICE_INIT_PARAMS, param_count
 
 
 @dataclass
@@ -197,7 +198,10 @@ class ImagePathExecutor:
             raise ProfileError(f"{spec.name}: no encoder configuration; the image path needs one")
         self.spec = spec
         self.device = torch.device(device)
-        self.weights = weights if weights is not None else init_weights(spec, seed)
+        if weights is None:
+            big = param_count(spec) > DEVICE_INIT_PARAMS and self.device.type == "cuda"
+            weights = init_weights(spec, seed, device=str(self.device) if big else "cpu")
+        self.weights = weights
         self.encoder = DeviceEncoder(spec, self.weights, self.device)
 
     # ------------------------------------------------------------------ core path

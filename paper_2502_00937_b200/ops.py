@@ -197,13 +197,51 @@ def gemm(a: torch.Tensor, b: torch.Tensor, epilogue: int = EPI_BF16, bias=None, 
     return out
 
 
-def ln_stats_finalize(stats, rows: int, d: int, eps: float, out=None):
-    """Folded LayerNorm: per-chunk (mean, M2) of the producer GEMM -> f32 [rows, 2] (mean, rstd)."""
+def ln_stats_finalize(stats, rows: int, d: int, eps: float, out=None, rms: bool = False):
+    """Folded LayerNorm: per-chunk (mean, M2) of the producer GEMM -> f32 [rows, 2] (mean, rstd);
+    ``rms``: RMSNorm statistics (0, 1/sqrt(mean(x^2) + eps))."""
     if out is None:
         out = torch.empty(rows, 2, dtype=torch.float32, device=stats.device)
     _t0 = _begin()
-    _lib.check(_lib.lib.mmk_ln_stats_finalize(stats.data_ptr(), rows, d, float(eps), out.data_ptr(), _s()))
+    _lib.check(_lib.lib.mmk_ln_stats_finalize(stats.data_ptr(), rows, d, float(eps), int(rms), out.data_ptr(), _s()))
     _end('layernorm', rows * (d // 32) * 8.0 + rows * 8.0, _t0)
+    return out
+
+
+def layernorm_bf16(x, gamma, beta, eps: float, out=None):
+    """Row LayerNorm of bf16 rows of any width (multiple of 8) -> bf16 (may be ``x`` itself)."""
+    _need_rows(x, torch.bfloat16, "x", x.shape[1])
+    if x.stride(0) != x.shape[1] or (out is not None and (out.shape != x.shape or not out.is_contiguous())):
+        raise SpecError("layernorm_bf16: contiguous rows required")
+    if out is None:
+        out = torch.empty_like(x)
+    _t0 = _begin()
+    _lib.check(_lib.lib.mmk_layernorm_bf16(x.data_ptr(), out.data_ptr(), x.shape[0], x.shape[1], gamma.data_ptr(),
+                                           beta.data_ptr(), float(eps), _s()))
+    _end('layernorm', x.numel() * 4.0, _t0)
+    return out
+
+
+def qk_rmsnorm(qkv, d: int, q_w, k_w, eps: float):
+    """InternViT QK-norm in place on the bf16 [Q | K | V] rows (RMSNorm over all heads of Q, of K)."""
+    _need_rows(qkv, torch.bfloat16, "qkv", 3 * d)
+    _t0 = _begin()
+    _lib.check(_lib.lib.mmk_qk_rmsnorm(qkv.data_ptr(), qkv.shape[0], d, qkv.stride(0), q_w.data_ptr(), k_w.data_ptr(),
+                                       float(eps), _s()))
+    _end('layernorm', qkv.shape[0] * 2 * d * 4.0, _t0)
+    return qkv
+
+
+def pack_pixel_shuffle(src, tiles: int, side: int, tokens_per_tile: int, drop: int, out=None):
+    """InternVL pixel shuffle (0.5) of each tile's fp32 patch rows -> bf16 [tiles*(side/2)^2, 4 d]."""
+    d = src.shape[1]
+    rows = tiles * (side // 2) ** 2
+    if out is None:
+        out = torch.empty(rows, 4 * d, dtype=torch.bfloat16, device=src.device)
+    _t0 = _begin()
+    _lib.check(_lib.lib.mmk_pack_pixel_shuffle(src.data_ptr(), tiles, side, tokens_per_tile, drop, d, out.data_ptr(),
+                                               _s()))
+    _end('pack', out.numel() * 4.0, _t0)
     return out
 
 
@@ -214,7 +252,7 @@ def layernorm(x, gamma, beta, eps: float, out=None, out_f32: bool = False, tile_
         out = torch.empty(rows, d, dtype=torch.float32 if out_f32 else torch.bfloat16, device=x.device)
     _t0 = _begin()
     _lib.check(_lib.lib.mmk_layernorm(x.data_ptr(), out.data_ptr(), int(out_f32), rows, d, gamma.data_ptr(),
-                                      beta.data_ptr(), float(eps), _p(tile_add), _p(tile_image), _p(image_table),
+                                      _p(beta), float(eps), _p(tile_add), _p(tile_image), _p(image_table),
                                       _p(tile_slot), rows_per_tile, slots, _s()))
     _end('layernorm', x.numel() * 4.0 + out.numel() * out.element_size(), _t0)
     return out

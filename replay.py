@@ -128,7 +128,7 @@ def main():
         if args.handoff == "peer":
             enc = spec.encoder
             P1 = spec.seq_per_tile
-            width = enc.hidden * (1 + len(enc.out_layers)) if enc.family == "mllama" else enc.hidden
+            width = enc.out_width
             chan = PeerShardChannel(rank, world, dev, torch.bfloat16, slot_rows=args.slot_images * spec.max_tiles_per_image * P1,
                                     width=width, **kw)
         else:

@@ -113,3 +113,44 @@ def test_clip_l336_full_depth():
     """Full 24-layer CLIP ViT-L/14-336 to layer -2 (LLaVA feature layer), CLS dropped."""
     from paper_2502_00937_b200 import core
     _run(core.get_model_spec("llava-clip-l14-336"), [(336, 336), (800, 600)], seed=3)
+
+
+def test_internvl_internvit_reduced_depth(monkeypatch):
+    """InternVL-26B / NVLM-D-72B's InternViT-6B at full width (d 3200, 25 heads of 128, FFN 12800)
+    and two layers: RMSNorm, QK-norm, layer scale folded into the O-proj / FC2, 448-px tiles with
+    a thumbnail (cap 5), class token dropped and the 32x32 grid pixel-shuffled to 256 tokens of
+    12800 channels; every tile its own sequence of 1025 tokens (hd-128 attention)."""
+    from paper_2502_00937_b200 import core
+    monkeypatch.setenv("MMK_LN_FOLD", "0")  # separate RMSNorm kernels (the folded path: next test)
+    spec = _reduced(core.get_model_spec("internvl-26b"), layers=2)
+    _run(spec, [(448, 448), (1000, 700), (300, 900)], seed=7)
+
+
+def test_internvl_folded_rmsnorm_path():
+    """The same with the RMSNorm folded into the GEMMs (the default for d >= 1024)."""
+    from paper_2502_00937_b200 import core
+    spec = _reduced(core.get_model_spec("nvlm-d-72b"), layers=3)
+    _run(spec, [(900, 900), (448, 300)], seed=8)
+
+
+@pytest.mark.parametrize("model", ["llama3.2-11b", "llava-ov-7b", "vit-b16-224"])
+def test_batch_invariance(model):
+    """An image's packed embedding is bit-identical whether it is encoded alone or inside a large
+    batch (kernel variants and the LN fold are chosen per encoder, never per batch size): the
+    property replay.py --verify relies on when it re-encodes a remote shard alone."""
+    from paper_2502_00937_b200 import core
+    from paper_2502_00937_b200.executor import ImagePathExecutor
+    spec = core.get_model_spec(model)
+    if spec.encoder.family == "mllama":
+        spec = _reduced(spec, layers=3, global_layers=1, out_layers=[1, 2])
+    else:
+        spec = _reduced(spec, layers=3)
+    rng = np.random.default_rng(9)
+    dims = [(1000, 700), (560, 560), (300, 2000)] * 4 + [(1500, 1500)] * 6
+    imgs = [rng.integers(0, 256, (h, w, 3), dtype=np.uint8) for w, h in dims]
+    ex = ImagePathExecutor(spec, seed=3)
+    big = ex.encode_images(imgs)
+    offs = big.tok_offsets.cpu().tolist()
+    for i in (0, 1, 2, len(imgs) - 1):
+        one = ex.encode_images([imgs[i]]).embeds
+        assert torch.equal(one, big.embeds[offs[i]:offs[i + 1]]), i

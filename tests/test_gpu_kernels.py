@@ -16,6 +16,7 @@ import torch
 
 pytestmark = pytest.mark.gpu
 
+from oracle import encoders as oenc  # noqa: E402
 from oracle import preprocess as oprep  # noqa: E402
 from oracle import tiling as otiling  # noqa: E402
 
@@ -144,7 +145,10 @@ def test_preprocess_thumbnail_spec_bit_exact(mk):
 
 # ----------------------------------------------------------------------------- GEMM
 @pytest.mark.parametrize("m,n,k", [(1, 256, 64), (129, 768, 592), (1576, 2304, 768), (5000, 3840, 1280),
-                                   (3000, 1280, 5120), (700, 1024, 4096), (20011, 1280, 640)])
+                                   (3000, 1280, 5120), (700, 1024, 4096), (20011, 1280, 640),
+                                   # CTA pairs with a partial last N tile (N % 256 = 128 / 64 / 192)
+                                   (20011, 3200, 1024), (20000, 1152, 576), (9000, 9600, 512),
+                                   (20000, 1344, 256), (19999, 1472, 320)])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3, 4])
 def test_gemm_epilogues(mk, m, n, k, epi):
     _, ops, _ = mk
@@ -169,6 +173,37 @@ def test_gemm_epilogues(mk, m, n, k, epi):
     out = ops.gemm(a, b, epi, bias=bias)
     tol = dict(rtol=1e-4, atol=1e-3) if epi == 3 else dict(rtol=1e-2, atol=2e-2)
     torch.testing.assert_close(out.float(), ref, **tol)
+
+
+@pytest.mark.parametrize("epi", [0, 3, 4])
+def test_gemm_partial_n_tile_writes_nothing_past_n(mk, epi):
+    """The CTA-pair kernel's partial last N tile (N = 3200 = 12.5 x 256) leaves every byte past
+    column N of the output, the bf16 copy and the LN statistics untouched (sentinel columns of
+    wider buffers; the next row's statistics follow directly)."""
+    _, ops, _ = mk
+    m, n, k, pad = 20011, 3200, 512, 64
+    a = torch.randn(m, k, device="cuda").bfloat16()
+    b = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
+    bias = torch.randn(n, device="cuda")
+    ref = a.float() @ b.float().t() + bias
+    if epi == 4:
+        big = torch.full((m, n + pad), 7.0, device="cuda")
+        base = torch.randn(m, n, device="cuda")
+        big[:, :n] = base
+        auxb = torch.full((m, n + pad), 3.0, device="cuda", dtype=torch.bfloat16)
+        stats = torch.full((m + 1, n // 32, 2), 5.0, device="cuda")
+        ops.gemm(a, b, 4, bias=bias, out=big[:, :n], gate=1.0, aux=auxb[:, :n], ln_stats_out=stats[:m])
+        torch.testing.assert_close(big[:, :n], base + ref, rtol=1e-4, atol=1e-3)
+        assert torch.all(big[:, n:] == 7.0) and torch.all(auxb[:, n:] == 3.0) and torch.all(stats[m] == 5.0)
+        v = (base + ref).view(m, n // 32, 32)
+        torch.testing.assert_close(stats[:m, :, 0], v.mean(-1), rtol=1e-4, atol=1e-4)
+        return
+    dt = torch.float32 if epi == 3 else torch.bfloat16
+    big = torch.full((m, n + pad), 9.0, device="cuda", dtype=dt)
+    ops.gemm(a, b, epi, bias=bias, out=big[:, :n])
+    tol = dict(rtol=1e-4, atol=1e-3) if epi == 3 else dict(rtol=1e-2, atol=2e-2)
+    torch.testing.assert_close(big[:, :n].float(), ref, **tol)
+    assert torch.all(big[:, n:] == 9.0)
 
 
 def test_gemm_strided_operands(mk):
@@ -210,7 +245,9 @@ def _attn_ref(qkv, lens, heads, hd):
                                            (64, 4, [(i * 37) % 701 for i in range(256)]),
                                            (64, 12, [197] * 300),                 # n_seq > 256: natural order
                                            (64, 2, [5] * 1000 + [577, 0, 1]),     # 1003 tiny sequences
-                                           (80, 1, [1601, 3202, 6404])])          # one head
+                                           (80, 1, [1601, 3202, 6404]),          # one head
+                                           (128, 4, [1025, 3, 2050, 0, 64]),     # hd 128 (InternViT)
+                                           (128, 25, [1025] * 40)])              # hd 128 persistent
 def test_attention_varlen(mk, hd, heads, lens):
     _, ops, _ = mk
     T = sum(lens)
@@ -454,7 +491,7 @@ def test_abi_status_codes_map_to_reference_exceptions(mk):
     qkv = torch.randn(10, 3 * 72, device="cuda").bfloat16()
     cu = torch.tensor([0, 10], dtype=torch.int32, device="cuda")
     with pytest.raises(ProfileError, match="head_dim"):
-        ops.attention(qkv, cu, 1, 10, 1, 72)
+        ops.attention(qkv, cu, 1, 10, 1, 72)  # padded to 80 by the encoder, never passed raw
     fin = torch.randn(8, 64, device="cuda")
     inter = torch.randn(9, 8, 64, device="cuda").bfloat16()
     with pytest.raises(ProfileError, match="n_inter"):
@@ -508,3 +545,93 @@ def test_layernorm_folded_into_gemms(mk, m, d, n, epi):
     out = ops.gemm(xr, wf, epi, bias=c2, ln_mr=mr, ln_c1=c1)
     rel = ((out.float() - ref).norm() / ref.norm()).item()
     assert rel < 1e-2, rel
+
+
+@pytest.mark.parametrize("m,d,n,epi", [(20011, 3200, 9600, 0), (5000, 3200, 12800, 1), (700, 256, 512, 0)])
+def test_rmsnorm_folded_into_gemms(mk, m, d, n, epi):
+    """InternViT's RMSNorm folded the same way: the finalize kernel's rms mode returns
+    (0, 1/sqrt(mean(x^2) + eps)), the consumer's c2 is the plain bias.  d = 3200 exercises the
+    single-CTA residual GEMM (N not a multiple of 256) emitting the statistics."""
+    _, ops, _ = mk
+    g = torch.Generator(device="cuda").manual_seed(m + n + 1)
+    resid = torch.randn(m, d, device="cuda", generator=g) * 2 + 0.5
+    h = (torch.randn(m, 256, device="cuda", generator=g)).bfloat16()
+    w2 = (torch.randn(d, 256, device="cuda", generator=g) * 0.05).bfloat16()
+    b2 = torch.randn(d, device="cuda", generator=g) * 0.1
+    gamma = 1 + 0.2 * torch.randn(d, device="cuda", generator=g)
+    w = (torch.randn(n, d, device="cuda", generator=g) * 0.05).bfloat16()
+    bias = torch.randn(n, device="cuda", generator=g) * 0.1
+    r_ref = resid + (h.float() @ w2.float().t() + b2)
+    x = r_ref * torch.rsqrt(r_ref.pow(2).mean(1, keepdim=True) + 1e-6) * gamma
+    ref = x @ w.float().t() + bias
+    if epi == 1:
+        ref = torch.nn.functional.gelu(ref)
+    xr = torch.empty(m, d, dtype=torch.bfloat16, device="cuda")
+    stats = torch.empty(m, d // 32, 2, device="cuda")
+    mr = torch.empty(m, 2, device="cuda")
+    r = resid.clone()
+    ops.gemm(h, w2, ops.EPI_RESID_F32, bias=b2, out=r, gate=1.0, aux=xr, ln_stats_out=stats)
+    ops.ln_stats_finalize(stats, m, d, 1e-6, out=mr, rms=True)
+    torch.testing.assert_close(r, r_ref, rtol=1e-4, atol=1e-3)
+    assert torch.all(mr[:, 0] == 0)
+    torch.testing.assert_close(mr[:, 1], torch.rsqrt(r_ref.pow(2).mean(1) + 1e-6), rtol=1e-4, atol=1e-5)
+    wf = (w.double() * gamma.double()[None, :]).bfloat16()
+    out = ops.gemm(xr, wf, epi, bias=bias, ln_mr=mr, ln_c1=wf.double().sum(1).float())
+    rel = ((out.float() - ref).norm() / ref.norm()).item()
+    assert rel < 1e-2, rel
+
+
+@pytest.mark.parametrize("d", [768, 1280, 3200])
+def test_rmsnorm_kernel(mk, d):
+    """mmk_layernorm with beta NULL is RMSNorm (InternVLVisionRMSNorm)."""
+    _, ops, _ = mk
+    x = torch.randn(1003, d, device="cuda") * 3 + 1
+    w = 1 + 0.1 * torch.randn(d, device="cuda")
+    got = ops.layernorm(x, w, None, 1e-6)
+    ref = x * torch.rsqrt(x.pow(2).mean(1, keepdim=True) + 1e-6) * w
+    torch.testing.assert_close(got.float(), ref, rtol=1e-2, atol=1e-2)
+    # bf16 output: at most 1 ulp off the correctly rounded fp32 result
+    assert (got.float() - ref.bfloat16().float()).abs().max() <= (ref.abs().max() * 2 ** -7)
+
+
+@pytest.mark.parametrize("d,ld_extra", [(3200, 0), (256, 64), (64, 8)])
+def test_qk_rmsnorm(mk, d, ld_extra):
+    """QK-norm in place on [Q | K | V] rows: Q and K each RMS-normalised over all d columns, V and
+    the row padding untouched."""
+    _, ops, _ = mk
+    rows = 1025 * 3
+    buf = (torch.randn(rows, 3 * d + ld_extra, device="cuda") * 2).bfloat16()
+    qkv = buf[:, :3 * d]
+    qw, kw = 1 + 0.1 * torch.randn(d, device="cuda"), 1 + 0.1 * torch.randn(d, device="cuda")
+    before = buf.clone()
+    ops.qk_rmsnorm(qkv, d, qw, kw, 1e-6)
+
+    def rms(t, w):
+        t = t.float()
+        return t * torch.rsqrt(t.pow(2).mean(1, keepdim=True) + 1e-6) * w
+    torch.testing.assert_close(buf[:, :d].float(), rms(before[:, :d], qw), rtol=1e-2, atol=2e-2)
+    torch.testing.assert_close(buf[:, d:2 * d].float(), rms(before[:, d:2 * d], kw), rtol=1e-2, atol=2e-2)
+    assert torch.equal(buf[:, 2 * d:], before[:, 2 * d:])
+
+
+@pytest.mark.parametrize("side,d,drop,tiles", [(32, 3200, 1, 3), (4, 64, 1, 5), (6, 8, 0, 2)])
+def test_pack_pixel_shuffle_matches_oracle(mk, side, d, drop, tiles):
+    """K9 for InternVL: bit-identical to the oracle's restatement of InternVLModel.pixel_shuffle
+    (pinned to transformers in tests/test_oracle_hf.py) on each tile, CLS dropped, bf16 out."""
+    _, ops, _ = mk
+    S = side * side + drop
+    src = torch.randn(tiles * S, d, device="cuda")
+    got = ops.pack_pixel_shuffle(src, tiles, side, S, drop).cpu()
+    h = src.cpu().view(tiles, S, d)[:, drop:]
+    ref = torch.cat([oenc.pixel_shuffle(h[t].contiguous(), side) for t in range(tiles)]).bfloat16()
+    assert got.shape == ref.shape and torch.equal(got, ref)
+
+
+@pytest.mark.parametrize("d", [12800, 4096, 8])
+def test_layernorm_bf16_wide_rows(mk, d):
+    _, ops, _ = mk
+    x = (torch.randn(257, d, device="cuda") * 2 + 0.3).bfloat16()
+    g, b = 1 + 0.1 * torch.randn(d, device="cuda"), 0.1 * torch.randn(d, device="cuda")
+    got = ops.layernorm_bf16(x, g, b, 1e-5)
+    ref = torch.nn.functional.layer_norm(x.float(), (d,), g, b, 1e-5)
+    torch.testing.assert_close(got.float(), ref, rtol=1e-2, atol=2e-2)

@@ -325,3 +325,75 @@ def test_siglip_vision_matches_hf():
     enc = SimpleNamespace(norm_eps=1e-6, layers=layers, heads=heads, act="gelu_tanh", drop_cls=False, out_layer=-1,
                           cls_token=False, pre_ln=False)
     torch.testing.assert_close(oenc.clip_image(patches, W, enc), hf, rtol=1e-4, atol=1e-4)
+
+
+@torch.no_grad()
+def test_internvit_and_pixel_shuffle_match_hf():
+    """InternViT-6B's structure (InternVL / NVLM presets): RMSNorm, QK-norm over the whole
+    projection, per-channel layer scale, no QKV bias but an output-projection bias, class token +
+    absolute positions; then InternVLModel.get_image_features' class-token drop and
+    pixel_shuffle(0.5) (the projector is not part of the emitted features)."""
+    from types import SimpleNamespace
+
+    from transformers import InternVLVisionConfig, InternVLVisionModel
+    from transformers.models.internvl.modeling_internvl import InternVLModel
+    d, ff, heads, layers, T, p = 64, 160, 2, 3, 56, 14  # 4x4 patch grid -> 2x2 shuffled tokens of 256
+    cfg = InternVLVisionConfig(hidden_size=d, intermediate_size=ff, num_attention_heads=heads, num_hidden_layers=layers,
+                               image_size=T, patch_size=p, use_qk_norm=True, norm_type="rms_norm", attention_bias=False,
+                               layer_norm_eps=1e-6, use_mean_pooling=True, hidden_act="gelu")
+    m = InternVLVisionModel(cfg).eval()
+    g = torch.Generator().manual_seed(11)
+    P = (T // p) ** 2
+    W = {"patch_w": 0.05 * torch.randn(d, 3 * p * p, generator=g), "patch_b": 0.1 * torch.randn(d, generator=g),
+         "cls": 0.5 * torch.randn(d, generator=g), "pos": torch.randn(P + 1, d, generator=g) * 0.1}
+    for i in range(layers):
+        pre = f"l{i}."
+        _rand_block(W, pre, d, ff, g, bias=False)
+        W[pre + "ln1_b"] = W[pre + "ln2_b"] = None  # RMSNorm
+        W[pre + "o_b"] = 0.05 * torch.randn(d, generator=g)
+        W[pre + "q_norm"] = 1 + 0.1 * torch.randn(d, generator=g)
+        W[pre + "k_norm"] = 1 + 0.1 * torch.randn(d, generator=g)
+        W[pre + "ls1"] = 0.5 + 0.1 * torch.randn(d, generator=g)
+        W[pre + "ls2"] = 0.5 + 0.1 * torch.randn(d, generator=g)
+    emb = m.embeddings
+    emb.patch_embeddings.projection.weight.data.copy_(W["patch_w"].view(d, 3, p, p))
+    emb.patch_embeddings.projection.bias.data.copy_(W["patch_b"])
+    emb.cls_token.data.copy_(W["cls"].view(1, 1, d))
+    emb.position_embeddings.data.copy_(W["pos"][None])
+    for i, layer in enumerate(m.encoder.layer):
+        pre, a = f"l{i}.", m.encoder.layer[i].attention
+        q, k, v = W[pre + "qkv_w"].split(d, 0)
+        a.q_proj.weight.data.copy_(q)
+        a.k_proj.weight.data.copy_(k)
+        a.v_proj.weight.data.copy_(v)
+        a.projection_layer.weight.data.copy_(W[pre + "o_w"])
+        a.projection_layer.bias.data.copy_(W[pre + "o_b"])
+        a.q_norm.weight.data.copy_(W[pre + "q_norm"])
+        a.k_norm.weight.data.copy_(W[pre + "k_norm"])
+        layer.layernorm_before.weight.data.copy_(W[pre + "ln1_w"])
+        layer.layernorm_after.weight.data.copy_(W[pre + "ln2_w"])
+        layer.lambda_1.data.copy_(W[pre + "ls1"])
+        layer.lambda_2.data.copy_(W[pre + "ls2"])
+        layer.mlp.fc1.weight.data.copy_(W[pre + "fc1_w"])
+        layer.mlp.fc1.bias.data.copy_(W[pre + "fc1_b"])
+        layer.mlp.fc2.weight.data.copy_(W[pre + "fc2_w"])
+        layer.mlp.fc2.bias.data.copy_(W[pre + "fc2_b"])
+    px = torch.randn(1, 3, T, T, generator=g)
+    feats = m(pixel_values=px).last_hidden_state[:, 1:]
+    side = T // p
+    hf = InternVLModel.pixel_shuffle(None, feats.reshape(1, side, side, d), 0.5).reshape(-1, 4 * d)
+    patches = px[0].unfold(1, p, p).unfold(2, p, p).permute(1, 2, 0, 3, 4).reshape(P, 3 * p * p)
+    enc = SimpleNamespace(norm_eps=1e-6, layers=layers, heads=heads, act="gelu", drop_cls=True, out_layer=-1,
+                          cls_token=True, pre_ln=False, pixel_shuffle=True)
+    torch.testing.assert_close(oenc.clip_image(patches, W, enc), hf, rtol=1e-4, atol=1e-4)
+
+
+def test_pixel_shuffle_column_order():
+    """The restated shuffle's token (y, x) is [f(2y,2x) | f(2y,2x+1) | f(2y+1,2x) | f(2y+1,2x+1)]."""
+    side, C = 6, 3
+    f = torch.arange(side * side * C, dtype=torch.float32).view(side * side, C)
+    out = oenc.pixel_shuffle(f, side)
+    for y in range(side // 2):
+        for x in range(side // 2):
+            want = torch.cat([f[(2 * y + i) * side + 2 * x + j] for i in (0, 1) for j in (0, 1)])
+            assert torch.equal(out[y * (side // 2) + x], want)
