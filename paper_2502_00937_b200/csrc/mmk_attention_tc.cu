@@ -62,6 +62,12 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #define MMK_ATTN_SPLIT 0
 #endif
 
+// K/V ring depth for hd 128 (64-key tiles of 32 KB): 3 fits beside the persistent kernel's two Q
+// slots once its longest-first schedule table is capped at 96 sequences (TcPersistLayout)
+#ifndef MMK_ATTN_HD128_STAGES
+#define MMK_ATTN_HD128_STAGES 3
+#endif
+
 template <int HD, int BKV, int NQ>
 struct TcAttnCfg {
   static constexpr bool kLSum = MMK_ATTN_LSUM && HD == 80;   // l accumulated by the tensor core
@@ -74,7 +80,7 @@ struct TcAttnCfg {
   static constexpr int kKVBlock = BKV * 64 * 2;              // one main block of K or V: BKV rows x 64 cols
   static constexpr int kKVMain = kBlocks * kKVBlock;
   static constexpr int kKVBytes = kKVMain + (kRem ? BKV * 16 * 2 : 0);
-  static constexpr int STAGES = HD > 80 ? 2 : 4;             // hd 128: the persistent kernel's two Q slots fill smem
+  static constexpr int STAGES = HD > 80 ? MMK_ATTN_HD128_STAGES : 4;
   static constexpr int kQOff = 0;
   static constexpr int kKVOff = NQ * kQBytes;
   static constexpr int kStageBytes = 2 * kKVBytes;           // K then V
@@ -706,11 +712,12 @@ struct AttnItem {
   int s_begin, len, q0, head, n_qt, nkv;  // len < 0: no more items
 };
 
-constexpr int kMaxSched = 256;
-
 template <int HD, int BKV, int NQ>
 struct TcPersistLayout {
   using C = TcAttnCfg<HD, BKV, NQ>;
+  // sequences the longest-first schedule can sort (more: natural order); hd 128 trades table
+  // space for a third K/V stage (InternViT's per-tile sequences are all 1025 tokens long anyway)
+  static constexpr int kMaxSched = HD > 80 ? 96 : 256;
   static constexpr int kQSlotBytes = NQ * C::kQBytes;
   static constexpr int kQOff = 0;                          // two Q slots
   static constexpr int kKVOff = 2 * kQSlotBytes;
@@ -761,6 +768,7 @@ attn_fwd_tc_persistent(const __grid_constant__ CUtensorMap tm_q, const __grid_co
 
   int n_items = qblocks * heads * n_seq;
   const int d_model = heads * HD;
+  constexpr int kMaxSched = Lay::kMaxSched;
   int* sch_len = reinterpret_cast<int*>(smem + Lay::kSchedOff);  // [kMaxSched]
   int* sch_order = sch_len + kMaxSched;                           // [kMaxSched] rank -> sequence
   int* sch_pre = sch_order + kMaxSched;                           // [kMaxSched + 1] items before rank
@@ -1059,7 +1067,7 @@ static int launch_attn_cfg(const void* qkv, void* out, const int32_t* cu, int n_
     const char* e = getenv("MMK_ATTN_LPT");
     return e ? atoi(e) != 0 : true;
   }();
-  const bool lpt = lpt_on && n_seq <= kMaxSched;
+  const bool lpt = lpt_on && n_seq <= TcPersistLayout<HD, BKV, NQ>::kMaxSched;
   const int persist_grid = static_cast<int>(n_items < num_sms() ? n_items : num_sms());  // one CTA per SM
   __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out);
   // workspace: [0] work-item counter of the main pass, [1] overflow flag, [2] counter of the exact redo
