@@ -1,12 +1,13 @@
 #!/bin/bash
 # Multi-GPU evidence on one box: weak-scaling bench lines N=1..N and the replay service (bursty trace
 # through route_image / form_batch, routing on the measured profile, fused NVLink handoff, connector,
-# every remote shard verified) at N=1, 2, N.   Usage: bash scripts/multi_run.sh N
+# every remote shard verified) at N=1, 2, N.   Usage: [SKIP_BENCH=1] bash scripts/multi_run.sh N
 set -u
 cd "$(dirname "$0")/.."
 N=${1:-4}
 O=gpurun_out
 for n in $(seq 1 $N); do
+  [ -n "${SKIP_BENCH:-}" ] && break
   if [ $n -eq 1 ]; then
     timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > $O/scale_r02b_weak_n1.json 2>$O/scale_r02b_weak_n1.err
   else

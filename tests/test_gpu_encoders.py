@@ -46,7 +46,11 @@ def _run(spec, dims, seed=0):
     scale, shift = oprep.norm_constants(enc.mean, enc.std)
     patches = oprep.bf16_bits_to_f32(oprep.preprocess(imgs, oplan, spec.tile_edge_px, enc.patch_px, k_pad_of(spec),
                                                       enc.resize_mode, spec.thumbnail_tile, scale, shift))
-    ref = oenc.encode(torch.from_numpy(patches), oplan, ex.weights, spec)
+    # the fp32 oracle runs where the weights live: the CPU, or the GPU for encoders whose weights
+    # are drawn there (InternViT-6B; torch fp32 matmuls, TF32 off)
+    wdev = ex.weights["patch_w"].device
+    assert not torch.backends.cuda.matmul.allow_tf32
+    ref = oenc.encode(torch.from_numpy(patches).to(wdev), oplan, ex.weights, spec).cpu()
     got = out.embeds.float().cpu()
     assert got.shape == ref.shape, (got.shape, ref.shape)
     assert out.tok_offsets.cpu().tolist() == oplan["tok_off"].tolist()
@@ -124,6 +128,13 @@ def test_internvl_internvit_reduced_depth(monkeypatch):
     monkeypatch.setenv("MMK_LN_FOLD", "0")  # separate RMSNorm kernels (the folded path: next test)
     spec = _reduced(core.get_model_spec("internvl-26b"), layers=2)
     _run(spec, [(448, 448), (1000, 700), (300, 900)], seed=7)
+
+
+def test_internvl_full_depth_gpu_oracle():
+    """Full 45-layer InternViT-6B (weights drawn on the GPU) against the fp32 oracle run with
+    torch on the same GPU: a 1-tile and a 5-tile (4 + thumbnail) image."""
+    from paper_2502_00937_b200 import core
+    _run(core.get_model_spec("internvl-26b"), [(448, 448), (900, 800)], seed=10)
 
 
 def test_internvl_folded_rmsnorm_path():
