@@ -136,6 +136,22 @@ MMK_DEV void chunk_stats(const float (&v)[32], float2* dst) {
   *dst = make_float2(mean, m2);
 }
 
+// Tile order of the persistent CTA-pair kernel: group_m = 1 is N-major (the ~74 clusters in
+// flight share ~1.5 A blocks, each streams its own weight tile); group_m > 1 walks down group_m M
+// blocks before moving to the next N tile, so in-flight clusters share ~group_m A blocks and
+// ~74/group_m weight tiles.  With InternViT's 61-82 MB weights the N-major order re-streamed them
+// from DRAM for every M block (7-15x the algorithmic bytes, ncu); grouping by 16 is +0.7 % there
+// and -1.5 % on Mllama's 3-13 MB weights (same box, alternating), hence the host's choice by
+// weight size.
+MMK_DEV void grouped_tile(int tile, int n_tiles_m, int n_tiles_n, int group_m, int& mb, int& nb) {
+  const int per_group = group_m * n_tiles_n;
+  const int first_m = (tile / per_group) * group_m;
+  const int gm = min(group_m, n_tiles_m - first_m);
+  const int local = tile - (tile / per_group) * per_group;
+  mb = first_m + local % gm;
+  nb = local / gm;
+}
+
 // Fused epilogue for 32 consecutive accumulator columns of one output row (thread-owned row).
 template <int EPI>
 MMK_DEV void epilogue_chunk(const uint32_t (&r)[32], int row, int col, const float* __restrict__ bias, void* out,
@@ -407,7 +423,7 @@ template <int STAGES, int EPI, bool RES_TMA = false>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                       const __grid_constant__ CUtensorMap tmap_out, int M, int N, int K, const float* __restrict__ bias, void* __restrict__ out, int64_t ldo,
-                      float gate, __nv_bfloat16* __restrict__ aux, int64_t ld_aux, LnFold lf) {
+                      float gate, __nv_bfloat16* __restrict__ aux, int64_t ld_aux, LnFold lf, int group_m) {
   using S = Gemm2Smem<STAGES>;
   constexpr int BN = kGemm2BN;
   extern __shared__ uint8_t smem_raw[];
@@ -426,7 +442,8 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
   // N % 64 == 0: the last N tile may be partial (InternViT d 3200, SigLIP 1152): B rows past N
   // load as zeros (TMA out-of-bounds fill), stores past N are clipped by the output map or skipped
   const int n_tiles_n = (N + BN - 1) / BN;
-  const int n_tiles = ((M + 255) / 256) * n_tiles_n;
+  const int n_tiles_m = (M + 255) / 256;
+  const int n_tiles = n_tiles_m * n_tiles_n;
   const int num_kb = (K + kGemmBK - 1) / kGemmBK;
   const int first = static_cast<int>(cluster_id_x()), step = static_cast<int>(n_clusters_x());
 
@@ -464,8 +481,10 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = first; tile < n_tiles; tile += step) {
-      const int m0 = (tile / n_tiles_n) * 256 + rank * 128;
-      const int n0 = (tile % n_tiles_n) * BN + rank * (BN / 2);
+      int mb, nb;
+      grouped_tile(tile, n_tiles_m, n_tiles_n, group_m, mb, nb);
+      const int m0 = mb * 256 + rank * 128;
+      const int n0 = nb * BN + rank * (BN / 2);
       for (int kb = 0; kb < num_kb; ++kb) {
         mbar_wait(&empty_bar[stage], phase ^ 1);
         uint8_t* sa = smem + stage * S::kStageBytes;
@@ -527,8 +546,10 @@ gemm_bf16_tcgen05_2sm(const __grid_constant__ CUtensorMap tmap_a, const __grid_c
     for (int tile = first; tile < n_tiles; tile += step, ++t) {
       const int acc = t & 1;
       const uint32_t acc_phase = (t >> 1) & 1;
-      const int m0 = (tile / n_tiles_n) * 256 + rank * 128;
-      const int n0 = (tile % n_tiles_n) * BN;
+      int mb, nb;
+      grouped_tile(tile, n_tiles_m, n_tiles_n, group_m, mb, nb);
+      const int m0 = mb * 256 + rank * 128;
+      const int n0 = nb * BN;
       if constexpr (RES_TMA) {
         // residual chunks 0 and 1 of this tile into the warp's two slots (chunks 2, 3 follow as
         // the slots drain); issued before waiting for the accumulator so they overlap the MMAs
@@ -755,7 +776,7 @@ template <int STAGES, int EPI, bool RES_TMA = false>
 static int launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, int M, int N, int K,
                            const float* bias,
                            void* out, int64_t ldo, float gate, __nv_bfloat16* aux, int64_t ld_aux,
-                           const LnFold& lf, cudaStream_t stream) {
+                           const LnFold& lf, int group_m, cudaStream_t stream) {
   using S = Gemm2Smem<STAGES>;
   auto kern = gemm_bf16_tcgen05_2sm<STAGES, EPI, RES_TMA>;
   static std::atomic<uint64_t> attr_done{0};  // per template instance
@@ -765,7 +786,7 @@ static int launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, const C
   const int pairs_max = num_sms() / 2;
   const int pairs = tiles < pairs_max ? tiles : pairs_max;
   cudaError_t e = launch_kernel(kern, dim3(2 * pairs), dim3(kGemmThreads), S::kTotal, stream, 2, tiles <= num_sms(), ta, tb, to, M, N, K,
-                                bias, out, ldo, gate, aux, ld_aux, lf);
+                                bias, out, ldo, gate, aux, ld_aux, lf, group_m);
   if (e != cudaSuccess) return set_cuda_error(e, "gemm2: launch");
   return MMK_OK;
 }
@@ -773,17 +794,17 @@ static int launch_gemm_2sm(const CUtensorMap& ta, const CUtensorMap& tb, const C
 template <int STAGES>
 static int dispatch_epi_2sm(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, int M,
                             int N, int K, const float* bias, void* out, int64_t ldo, float gate,
-                            __nv_bfloat16* aux, int64_t ld_aux, const LnFold& lf, cudaStream_t s) {
+                            __nv_bfloat16* aux, int64_t ld_aux, const LnFold& lf, int g, cudaStream_t s) {
   switch (epi) {
-    case MMK_EPI_BF16: return launch_gemm_2sm<STAGES, MMK_EPI_BF16>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
-    case MMK_EPI_BF16_GELU: return launch_gemm_2sm<STAGES, MMK_EPI_BF16_GELU>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
-    case MMK_EPI_BF16_QUICKGELU: return launch_gemm_2sm<STAGES, MMK_EPI_BF16_QUICKGELU>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
-    case MMK_EPI_BF16_GELU_TANH: return launch_gemm_2sm<STAGES, MMK_EPI_BF16_GELU_TANH>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
-    case MMK_EPI_F32: return launch_gemm_2sm<STAGES, MMK_EPI_F32>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
+    case MMK_EPI_BF16: return launch_gemm_2sm<STAGES, MMK_EPI_BF16>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, g, s);
+    case MMK_EPI_BF16_GELU: return launch_gemm_2sm<STAGES, MMK_EPI_BF16_GELU>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, g, s);
+    case MMK_EPI_BF16_QUICKGELU: return launch_gemm_2sm<STAGES, MMK_EPI_BF16_QUICKGELU>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, g, s);
+    case MMK_EPI_BF16_GELU_TANH: return launch_gemm_2sm<STAGES, MMK_EPI_BF16_GELU_TANH>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, g, s);
+    case MMK_EPI_F32: return launch_gemm_2sm<STAGES, MMK_EPI_F32>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, g, s);
     case MMK_EPI_RESID_F32:
       // the fp32 residual streams through shared memory by TMA (O-proj 0.420 -> 0.365 ms, FC2
       // 1.165 -> 1.137 ms versus a direct read-modify-write from the epilogue registers)
-      return launch_gemm_2sm<STAGES, MMK_EPI_RESID_F32, true>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, s);
+      return launch_gemm_2sm<STAGES, MMK_EPI_RESID_F32, true>(ta, tb, to, M, N, K, bias, out, ldo, gate, aux, ld_aux, lf, g, s);
     default: return set_error(MMK_ERR_ARG, "gemm: unknown epilogue %d", epi);
   }
 }
@@ -838,8 +859,11 @@ extern "C" int mmk_gemm_bf16_ln(const void* a, int64_t lda, const void* b, int64
       rc = make_tmap(&to, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, out, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
       if (rc) return rc;
     }
+    // grouped tile order only for large weight matrices (see grouped_tile)
+    static const int group_env = getenv("MMK_GEMM_GROUP_M") ? atoi(getenv("MMK_GEMM_GROUP_M")) : 0;
+    const int group_m = group_env > 0 ? group_env : (static_cast<int64_t>(n) * k * 2 > (32ll << 20) ? 16 : 1);
     return dispatch_epi_2sm<5>(epilogue, ta, tb, to, m, n, k, bias, out, ldo, gate,
-                               reinterpret_cast<__nv_bfloat16*>(aux), ld_aux, lf, stream);
+                               reinterpret_cast<__nv_bfloat16*>(aux), ld_aux, lf, group_m, stream);
   }
   const int tiles256 = ((m + kGemmBM - 1) / kGemmBM) * ((n + 255) / 256);
   const bool use128 = (n % 256 != 0) || tiles256 < num_sms();
