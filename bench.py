@@ -439,22 +439,17 @@ def main():
     # leave them); every step copies them to the device inside the timed region
     pinned_imgs = [torch.from_numpy(np.ascontiguousarray(im)).pin_memory() for im in imgs]
     ck = torch.empty(1, device="cuda")
-    for _ in range(1):
-        o = ex.encode_images(pinned_imgs)
+    for _ in range(2):  # a shape seen twice is captured by encode_images (outside the timed region)
+        o = ex.encode_images(pinned_imgs, out_alloc=out_alloc)
         ops.checksum(o.embeds, out=ck)
     barrier()
     h2d = d2h = 0
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     e_start.record(stream)
-    copy_stream = torch.cuda.Stream()
-    b_next = stage_images(pinned_imgs, stream=copy_stream)
     for s_i in range(args.steps):
-        b = b_next
-        if s_i + 1 < args.steps:  # the next step's H2D overlaps this step's encode
-            b_next = stage_images(pinned_imgs, stream=copy_stream)
-        o = ex.encode(b, out_alloc=out_alloc)
-        h2d += b.h2d_bytes
+        o = ex.encode_images(pinned_imgs, out_alloc=out_alloc)
+        h2d += sum(t_.numel() for t_ in pinned_imgs) + 16 * len(pinned_imgs)
         if handoff is not None:
             handoff.send(o, sizes=rank_rows)
         ops.checksum(o.embeds, out=ck)
@@ -606,8 +601,9 @@ def main():
             "gpu_launches": launches,
             "e2e": {"value": round(e_value, 3), "unit": "images/s", "h2d_bytes_per_step": h2d // args.steps,
                     "d2h_bytes_per_step": d2h // args.steps,
-                    "path": ("ImagePathExecutor.encode(stage_images(pinned host uint8 images, per-image H2D on a side "
-                             "stream, next step staged during the current encode)) + checksum D2H")},
+                    "path": ("ImagePathExecutor.encode_images(pinned host uint8 images): per-image H2D, then the "
+                             "batch shape's captured graph replayed (eager launches with a peer out_alloc) + "
+                             "token offsets and checksum D2H")},
             "e2e_graph": e2e_graph,
             "e2e_jpeg": e2e_jpeg,
             "clocks": clk.result(),

@@ -14,6 +14,7 @@ token offsets — exactly ``Request.total_image_tokens`` rows (core.py:110-112) 
 
 from __future__ import annotations
 
+from collections import OrderedDict
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -139,6 +140,42 @@ class CapturedEncode:
         return self.output
 
 
+class _GraphEntry:
+    """One cached batch shape: the staged input buffer, the captured K0..K9 graph and its output.
+    ``run`` copies new pixels into the input buffer (per-image H2D from pinned tensors, or one H2D
+    from a page-locked staging copy) and replays; the returned tensors are fresh copies, so a
+    result never changes under its holder when the shape is encoded again."""
+
+    def __init__(self, ex: "ImagePathExecutor", imgs: list):
+        self.sizes = [int(im.shape[0]) * int(im.shape[1]) * 3 for im in imgs]
+        self.offs = np.concatenate([[0], np.cumsum(self.sizes)]).astype(np.int64)
+        self.host = None       # page-locked staging copy for host arrays (lazily)
+        self.copied = None     # event after the last H2D out of ``host``
+        self.cap = ex.capture(stage_images(imgs, ex.device))
+
+    def run(self, imgs: list) -> PackedBatch:
+        src = self.cap.batch.src
+        if all(isinstance(i, torch.Tensor) and i.device.type == "cpu" and i.is_pinned() and i.is_contiguous()
+               for i in imgs):
+            for i, im in enumerate(imgs):
+                src[self.offs[i]:self.offs[i + 1]].copy_(im.view(-1), non_blocking=True)
+        else:
+            if self.host is None:
+                self.host = torch.empty(int(self.offs[-1]), dtype=torch.uint8, pin_memory=True)
+            if self.copied is not None:
+                self.copied.synchronize()  # the previous H2D out of the staging copy has finished
+            hv = self.host.numpy()
+            for i, im in enumerate(imgs):
+                a = im.cpu().numpy() if isinstance(im, torch.Tensor) else im
+                hv[self.offs[i]:self.offs[i + 1]] = a.reshape(-1)
+            src.copy_(self.host, non_blocking=True)
+            self.copied = torch.cuda.Event()
+            self.copied.record()
+        o = self.cap.replay()
+        return PackedBatch(embeds=o.embeds.clone(), tok_offsets=o.tok_offsets.clone(), tiles=list(o.tiles),
+                           image_tokens=list(o.image_tokens))
+
+
 JPEG_DECODE_CHUNK = 32
 _DECODE_STREAMS: dict = {}
 
@@ -192,7 +229,13 @@ def stage_jpegs(jpegs, device="cuda") -> ImageBatch:
 class ImagePathExecutor:
     """preprocess -> encode -> pack for one model on one GPU (one process per GPU)."""
 
-    def __init__(self, spec: ModelSpec, weights: dict | None = None, seed: int = 0, device="cuda"):
+    # batch shapes (the images' sizes, in order) kept as captured CUDA graphs by encode_images: a
+    # shape seen twice is captured, replays then skip the per-kernel launch cost (ViT-B batch 8 is
+    # a ~1 ms step of ~120 launches); least recently used shapes are dropped beyond this many
+    GRAPH_CACHE_SHAPES = 4
+
+    def __init__(self, spec: ModelSpec, weights: dict | None = None, seed: int = 0, device="cuda",
+                 graphs: bool = True):
         if spec.encoder is None:
             from ._lib import ProfileError
             raise ProfileError(f"{spec.name}: no encoder configuration; the image path needs one")
@@ -203,6 +246,9 @@ class ImagePathExecutor:
             weights = init_weights(spec, seed, device=str(self.device) if big else "cpu")
         self.weights = weights
         self.encoder = DeviceEncoder(spec, self.weights, self.device)
+        self.graphs = graphs and self.device.type == "cuda"
+        self._graph_cache: OrderedDict = OrderedDict()  # shape -> _GraphEntry
+        self._shape_seen: dict = {}
 
     # ------------------------------------------------------------------ core path
     def encode(self, batch: ImageBatch, out_alloc=None) -> PackedBatch:
@@ -257,7 +303,27 @@ class ImagePathExecutor:
         return CapturedEncode(graph=g, batch=batch, output=out)
 
     def encode_images(self, images, pinned: bool = True, out_alloc=None) -> PackedBatch:
-        return self.encode(stage_images(images, self.device, pinned), out_alloc=out_alloc)
+        """uint8 HWC images (host arrays, or pinned host tensors) -> packed embeddings.  A batch
+        shape seen before runs as a replay of its captured graph (``graphs``; not with
+        ``out_alloc``, whose destination may change per call)."""
+        if not (self.graphs and pinned and out_alloc is None):
+            return self.encode(stage_images(images, self.device, pinned), out_alloc=out_alloc)
+        imgs = [_as_hwc_u8(i) for i in images]
+        key = tuple((int(i.shape[1]), int(i.shape[0])) for i in imgs)
+        entry = self._graph_cache.get(key)
+        if entry is None:
+            seen = self._shape_seen.get(key, 0) + 1
+            if len(self._shape_seen) > 4096:
+                self._shape_seen.clear()
+            self._shape_seen[key] = seen
+            if seen < 2 or not imgs:
+                return self.encode(stage_images(imgs, self.device, pinned))
+            entry = _GraphEntry(self, imgs)
+            self._graph_cache[key] = entry
+            while len(self._graph_cache) > self.GRAPH_CACHE_SHAPES:
+                self._graph_cache.popitem(last=False)
+        self._graph_cache.move_to_end(key)
+        return entry.run(imgs)
 
     def encode_jpegs(self, jpegs) -> PackedBatch:
         """JPEG bytes -> GPU decode -> K0..K9 (no host pixel handling at all)."""

@@ -301,6 +301,10 @@ class ImagePathService:
                  policies: pol.PolicySet | None = None, max_batch: dict | None = None, cost_ms=None,
                  ttft_slo_ms: float = 1e9, connector=None):
         self.spec, self.executor, self.rank, self.world = spec, executor, rank, world
+        if executor is not None:
+            # no graph capture under the service: receiver threads launch work concurrently (a
+            # capture would see their launches) and trace batches rarely repeat a shape
+            executor.graphs = False
         self.policies = policies or pol.PolicySet()
         self.max_batch = max_batch or {StageKind.ENCODE.value: 8}
         self.cost_ms = cost_ms or (lambda tiles: 10.0 * tiles)

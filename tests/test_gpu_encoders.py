@@ -165,3 +165,27 @@ def test_batch_invariance(model):
     for i in (0, 1, 2, len(imgs) - 1):
         one = ex.encode_images([imgs[i]]).embeds
         assert torch.equal(one, big.embeds[offs[i]:offs[i + 1]]), i
+
+
+def test_encode_images_graph_cache():
+    """A batch shape seen twice runs as a captured graph: new pixels of the same shape give the
+    eager path's bit-identical embeddings, returned tensors are independent copies, a new shape
+    falls back to the eager path, and pinned-tensor and host-array inputs both work."""
+    from paper_2502_00937_b200 import core
+    from paper_2502_00937_b200.executor import ImagePathExecutor
+    spec = _reduced(core.get_model_spec("vit-b16-224"), layers=2)
+    ex = ImagePathExecutor(spec, seed=1)
+    eager = ImagePathExecutor(spec, weights=ex.weights, graphs=False)
+    rng = np.random.default_rng(3)
+    dims = [(224, 224)] * 3 + [(300, 500)]
+    batches = [[rng.integers(0, 256, (h, w, 3), dtype=np.uint8) for w, h in dims] for _ in range(4)]
+    outs = []
+    for i, b in enumerate(batches):
+        inp = [torch.from_numpy(a).pin_memory() for a in b] if i % 2 else b
+        outs.append(ex.encode_images(inp))
+    assert len(ex._graph_cache) == 1
+    for b, o in zip(batches, outs):
+        ref = eager.encode_images(b)
+        assert torch.equal(o.embeds, ref.embeds) and torch.equal(o.tok_offsets, ref.tok_offsets)
+    other = ex.encode_images(batches[0][:2])
+    assert torch.equal(other.embeds, eager.encode_images(batches[0][:2]).embeds)
