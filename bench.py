@@ -126,6 +126,23 @@ def encoder_flops(spec, tiles_list):
     return tot
 
 
+def attention_exp_roofline(a, spec, clocks):
+    """The attention's other bound: one exponential per score, 7 of every 8 on MUFU.EX2 (16 per
+    clock per SM on B200: 8 cycles per warp instruction per sub-partition, scripts/micro/pipes.cu),
+    1 of 8 on an FMA-pipe polynomial (speculative tiles).  MUFU ops/s achieved vs 16 x SMs x the
+    median SM clock sampled during the timed region."""
+    import torch
+    if not a.get("ms") or not clocks.get("sm_mhz"):
+        return None
+    scores = a["work"] / (4.0 * spec.encoder.head_dim)  # work = 4 S^2 H hd with the model's head_dim
+    mufu = scores * 7.0 / 8.0 / (a["ms"] / 1e3)
+    peak = 16.0 * torch.cuda.get_device_properties(0).multi_processor_count * clocks["sm_mhz"] * 1e6
+    return {"bound": "mufu", "achieved": round(mufu / 1e12, 3), "peak": round(peak / 1e12, 3), "unit": "Tops/s",
+            "frac": round(mufu / peak, 4),
+            "note": "exponentials of the attention (one per score, 7/8 on MUFU.EX2) per second vs the MUFU rate "
+                    "at the sampled median SM clock"}
+
+
 class ClockSampler:
     """nvidia-smi-equivalent clock / throttle sampling (NVML) during the timed region."""
 
@@ -571,6 +588,7 @@ def main():
                     "launches": k["launches"], "share_of_step": round(k["ms"] / ms_instr, 4) if ms_instr else None,
                     "timing": "per-launch CUDA events, eager repeat of the timed steps"}
 
+        clocks = clk.result()
         enc_tf = flops_job / world / (step_ms / 1e3) / 1e12  # per GPU
         line = {
             "metric": "images/sec (preprocess+encode)", "value": round(value, 3), "unit": "images/s",
@@ -592,6 +610,7 @@ def main():
             "roofline_step": {"achieved": round(enc_tf, 1), "peak": sus, "unit": "TFLOP/s",
                               "frac": round(enc_tf / sus, 4),
                               "note": "algorithmic encoder FLOPs of the whole step / step time"},
+            "roofline_attention_exp": attention_exp_roofline(a, spec, clocks),
             "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
                             "achieved": round(v["work"] / (v["ms"] / 1e3) /
                                               (1e12 if (k in ("gemm", "attention") or k.startswith("gemm.")) else 1e9), 1)
@@ -606,7 +625,7 @@ def main():
                              "token offsets and checksum D2H")},
             "e2e_graph": e2e_graph,
             "e2e_jpeg": e2e_jpeg,
-            "clocks": clk.result(),
+            "clocks": clocks,
         }
         if not args.no_cpu_baseline and world == 1:
             w_cpu = {k: (v.cpu() if isinstance(v, torch.Tensor) else v) for k, v in ex.weights.items()}

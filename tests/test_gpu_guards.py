@@ -72,8 +72,70 @@ def test_gemm_guards(mk):
         assert torch.equal(out, ref_out) and torch.equal(aux, ref_aux)
 
 
+def test_gemm_partial_n_tile_guards(mk):
+    """CTA-pair GEMM with a partial last N tile (N = 3200, 1152) and the LN-statistics output."""
+    _, ops, _ = mk
+    for m, n, k in ((20011, 3200, 512), (20000, 1152, 576)):
+        a = torch.randn(m, k, device="cuda").bfloat16()
+        b = (torch.randn(n, k, device="cuda") * 0.05).bfloat16()
+        bias = torch.randn(n, device="cuda")
+        ap, bp, biasp = _padded_input(a), _padded_input(b), _padded_input(bias)
+        for epi in (0, 1, 3):
+            ref = ops.gemm(a, b, epi, bias=bias)
+            full, out = _guarded((m, n), ref.dtype, -7.0)
+            ops.gemm(ap, bp, epi, bias=biasp, out=out)
+            torch.cuda.synchronize()
+            assert _guards_intact(full, m * n, -7.0) and torch.equal(out, ref), (m, n, epi)
+        base = torch.randn(m, n, device="cuda")
+        r_out, r_aux = base.clone(), torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
+        r_st = torch.empty(m, n // 32, 2, device="cuda")
+        ops.gemm(a, b, 4, bias=bias, out=r_out, gate=0.5, aux=r_aux, ln_stats_out=r_st)
+        full, out = _guarded((m, n), torch.float32, -7.0)
+        out.copy_(base)
+        afull, aux = _guarded((m, n), torch.bfloat16, -7.0)
+        sfull, st = _guarded((m, n // 32, 2), torch.float32, -7.0)
+        ops.gemm(ap, bp, 4, bias=biasp, out=out, gate=0.5, aux=aux, ln_stats_out=st)
+        torch.cuda.synchronize()
+        assert _guards_intact(full, m * n, -7.0) and _guards_intact(afull, m * n, -7.0)
+        assert _guards_intact(sfull, m * (n // 32) * 2, -7.0)
+        assert torch.equal(out, r_out) and torch.equal(aux, r_aux) and torch.equal(st, r_st)
+
+
+def test_internvit_kernels_guards(mk):
+    """QK-norm, RMSNorm, the pixel-shuffle pack and the wide bf16 LayerNorm."""
+    _, ops, _ = mk
+    d, rows = 3200, 2 * 1025
+    qkv = (torch.randn(rows, 3 * d, device="cuda") * 2).bfloat16()
+    qw, kw = 1 + 0.1 * torch.randn(d, device="cuda"), 1 + 0.1 * torch.randn(d, device="cuda")
+    ref = ops.qk_rmsnorm(qkv.clone(), d, qw, kw, 1e-6)
+    full, mid = _guarded((rows, 3 * d), torch.bfloat16, -7.0)
+    mid.copy_(qkv)
+    ops.qk_rmsnorm(mid, d, _padded_input(qw), _padded_input(kw), 1e-6)
+    torch.cuda.synchronize()
+    assert _guards_intact(full, rows * 3 * d, -7.0) and torch.equal(mid, ref)
+    x = torch.randn(rows, d, device="cuda")
+    ref = ops.layernorm(x, qw, None, 1e-6)
+    full, out = _guarded((rows, d), torch.bfloat16, -7.0)
+    ops.layernorm(_padded_input(x), _padded_input(qw), None, 1e-6, out=out)
+    torch.cuda.synchronize()
+    assert _guards_intact(full, rows * d, -7.0) and torch.equal(out, ref)
+    src = torch.randn(3 * 1025, d, device="cuda")
+    ref = ops.pack_pixel_shuffle(src, 3, 32, 1025, 1)
+    full, out = _guarded((3 * 256, 4 * d), torch.bfloat16, -7.0)
+    ops.pack_pixel_shuffle(_padded_input(src), 3, 32, 1025, 1, out=out)
+    torch.cuda.synchronize()
+    assert _guards_intact(full, 3 * 256 * 4 * d, -7.0) and torch.equal(out, ref)
+    xb = torch.randn(300, 4 * d, device="cuda").bfloat16()
+    g, b = torch.randn(4 * d, device="cuda"), torch.randn(4 * d, device="cuda")
+    ref = ops.layernorm_bf16(xb, g, b, 1e-5)
+    full, out = _guarded((300, 4 * d), torch.bfloat16, -7.0)
+    ops.layernorm_bf16(_padded_input(xb), _padded_input(g), _padded_input(b), 1e-5, out=out)
+    torch.cuda.synchronize()
+    assert _guards_intact(full, 300 * 4 * d, -7.0) and torch.equal(out, ref)
+
+
 @pytest.mark.parametrize("hd,heads,lens", [(80, 16, [1601, 3202, 1, 63]), (80, 16, [1601] * 24 + [6404] * 2),
-                                           (64, 16, [577] * 40 + [0, 5])])
+                                           (64, 16, [577] * 40 + [0, 5]), (128, 25, [1025] * 40 + [3, 0])])
 def test_attention_guards(mk, hd, heads, lens):
     _, ops, _ = mk
     T = sum(lens)

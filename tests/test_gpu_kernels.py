@@ -247,7 +247,9 @@ def _attn_ref(qkv, lens, heads, hd):
                                            (64, 2, [5] * 1000 + [577, 0, 1]),     # 1003 tiny sequences
                                            (80, 1, [1601, 3202, 6404]),          # one head
                                            (128, 4, [1025, 3, 2050, 0, 64]),     # hd 128 (InternViT)
-                                           (128, 25, [1025] * 40)])              # hd 128 persistent
+                                           (128, 25, [1025] * 40),               # hd 128 persistent
+                                           (128, 2, [(i * 37) % 701 for i in range(96)]),   # hd 128 LPT table full
+                                           (128, 2, [(i * 37) % 701 for i in range(120)])])  # > 96: natural order
 def test_attention_varlen(mk, hd, heads, lens):
     _, ops, _ = mk
     T = sum(lens)
