@@ -235,7 +235,10 @@ class ImagePathExecutor:
     GRAPH_CACHE_SHAPES = 4
 
     def __init__(self, spec: ModelSpec, weights: dict | None = None, seed: int = 0, device="cuda",
-                 graphs: bool = True):
+                 graphs: bool = True, fold_ln: bool | None = None):
+        """fold_ln: LayerNorms folded into the GEMMs (default: for encoders with d >= 1024; a narrow
+        encoder served at large batches gains from it too).  Fixed per executor, so embeddings
+        never depend on the batch an image is encoded in."""
         if spec.encoder is None:
             from ._lib import ProfileError
             raise ProfileError(f"{spec.name}: no encoder configuration; the image path needs one")
@@ -245,7 +248,7 @@ class ImagePathExecutor:
             big = param_count(spec) > DEVICE_INIT_PARAMS and self.device.type == "cuda"
             weights = init_weights(spec, seed, device=str(self.device) if big else "cpu")
         self.weights = weights
-        self.encoder = DeviceEncoder(spec, self.weights, self.device)
+        self.encoder = DeviceEncoder(spec, self.weights, self.device, fold_ln=fold_ln)
         self.graphs = graphs and self.device.type == "cuda"
         self._graph_cache: OrderedDict = OrderedDict()  # shape -> _GraphEntry
         self._shape_seen: dict = {}
