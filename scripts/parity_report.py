@@ -1,6 +1,7 @@
 """Parity report: the CUDA path against the fp32 CPU oracle at full model depth, per image
 (relative L2 error of the packed embeddings; tolerance 1e-2), plus the bit-exact checks of K0 / K1.
-Prints one JSON object (profiles/r01_parity.json)."""
+Prints one JSON object (profiles/r02/r02_parity.json).  InternViT-6B's weights are drawn on the GPU
+(5.5 B parameters), so its fp32 oracle runs with torch on the GPU (TF32 off)."""
 import json, os, sys, time
 import numpy as np
 import torch
@@ -15,7 +16,9 @@ report = {"tolerance": 1e-2, "metric": "per-image ||y - y_oracle|| / ||y_oracle|
           "weights": "random init (seeded), Mllama gates randomised", "configs": {}}
 cases = {"llama3.2-11b": [(560, 560), (1000, 500), (1400, 900), (1120, 1120)],
          "llava-clip-l14-336": [(336, 336), (800, 600), (300, 1000)],
-         "vit-b16-224": [(224, 224)] * 4}
+         "vit-b16-224": [(224, 224)] * 4,
+         "llava-ov-7b": [(384, 384), (1000, 700), (700, 1400)],
+         "internvl-26b": [(448, 448), (900, 800), (1300, 500)]}
 for name, dims in cases.items():
     spec = core.get_model_spec(name)
     enc = spec.encoder
@@ -36,7 +39,8 @@ for name, dims in cases.items():
                               int(plan["tile_off"][-1]), spec, k_pad_of(spec), torch.from_numpy(scale).cuda(),
                               torch.from_numpy(shift).cuda()).view(torch.int16).cpu().numpy().view(np.uint16)
     t0 = time.time()
-    ref = oenc.encode(torch.from_numpy(oprep.bf16_bits_to_f32(ref_bits)), plan, ex.weights, spec)
+    wdev = ex.weights["patch_w"].device
+    ref = oenc.encode(torch.from_numpy(oprep.bf16_bits_to_f32(ref_bits)).to(wdev), plan, ex.weights, spec).cpu()
     got = out.embeds.float().cpu()
     offs = plan["tok_off"]
     rel = []
@@ -48,6 +52,7 @@ for name, dims in cases.items():
         "tok_offsets_equal": out.tok_offsets.cpu().tolist() == plan["tok_off"].tolist(),
         "preprocess_bf16_mismatches": int((dev_bits != ref_bits).sum()), "preprocess_values": int(ref_bits.size),
         "rel_err_per_image": [round(r, 6) for r in rel], "max_rel_err": round(max(rel), 6),
-        "oracle_cpu_s": round(time.time() - t0, 1), "layers": enc.layers + getattr(enc, "global_layers", 0)}
+        "oracle_s": round(time.time() - t0, 1), "oracle_device": str(wdev),
+        "layers": enc.layers + getattr(enc, "global_layers", 0)}
     print(name, report["configs"][name], file=sys.stderr, flush=True)
 print(json.dumps(report))
