@@ -637,3 +637,22 @@ def test_layernorm_bf16_wide_rows(mk, d):
     got = ops.layernorm_bf16(x, g, b, 1e-5)
     ref = torch.nn.functional.layer_norm(x.float(), (d,), g, b, 1e-5)
     torch.testing.assert_close(got.float(), ref, rtol=1e-2, atol=2e-2)
+
+
+@pytest.mark.parametrize("d", [160, 768, 1280, 3200])
+@pytest.mark.parametrize("rms", [False, True])
+def test_ln_stats_finalize_forms(mk, d, rms):
+    """Both finalize forms (thread per row for an even chunk count, warp per row for an odd one:
+    d = 160 has 5 chunks) merge per-chunk (mean, M2) into the row's statistics."""
+    _, ops, _ = mk
+    rows = 5003
+    x = torch.randn(rows, d, device="cuda", dtype=torch.float64) * 3 + 0.7
+    c = x.view(rows, d // 32, 32)
+    stats = torch.stack([c.mean(-1), ((c - c.mean(-1, keepdim=True)) ** 2).sum(-1)], -1).float().contiguous()
+    mr = ops.ln_stats_finalize(stats, rows, d, 1e-5, rms=rms)
+    if rms:
+        want = torch.stack([torch.zeros(rows, device="cuda", dtype=torch.float64),
+                            torch.rsqrt(x.pow(2).mean(1) + 1e-5)], -1)
+    else:
+        want = torch.stack([x.mean(1), torch.rsqrt(x.var(1, unbiased=False) + 1e-5)], -1)
+    torch.testing.assert_close(mr.double(), want, rtol=2e-5, atol=2e-5)
