@@ -142,3 +142,51 @@ def test_form_batch_rules():  # reference test_engine.py:226-253
     q = [_item(0, StageKind.ENCODE, deps={99}), _item(1, StageKind.ENCODE)]
     assert batcher.form_batch(q, 10.0, policies.SchedulerKind.FIFO, 0.5, {"encode": 2}) == [1]
     assert batcher.form_batch([], 0.0, policies.SchedulerKind.FIFO, 0.5, {}) == []
+
+
+def test_encoder_blocks_of_every_reference_preset():
+    """Every reference preset carries an encoder whose emitted tokens per tile match the preset's
+    tokens_per_tile, and the packed row width the LLM side receives."""
+    widths = {"llama3.2-11b": 7680, "llama3.2-90b": 7680, "llava-ov-7b": 1152, "llava-ov-72b": 1152,
+              "internvl-26b": 12800, "nvlm-d-72b": 12800}
+    for name, width in widths.items():
+        spec = core.get_model_spec(name)
+        assert spec.encoder is not None, name
+        assert spec.encoder.out_width == width, name
+    iv = core.get_model_spec("internvl-26b").encoder
+    assert (iv.norm, iv.qk_norm, iv.layer_scale, iv.pixel_shuffle, iv.head_dim) == ("rms", True, True, True, 128)
+    assert iv.has_proj_bias and not iv.qkv_bias
+    assert core.get_model_spec("internvl-26b").seq_per_tile == 1025
+
+
+def test_encoder_spec_validation():
+    base = dict(family="clip", patch_px=14, hidden=64, ffn=128, layers=2, heads=2)
+    with pytest.raises(SpecError):
+        core.EncoderSpec(**base, norm="batch")
+    with pytest.raises(SpecError):  # the shuffle drops the class token first
+        core.EncoderSpec(**base, pixel_shuffle=True, drop_cls=False)
+    with pytest.raises(SpecError):
+        core.EncoderSpec(**{**base, "family": "mllama"}, norm="rms")
+    enc = core.EncoderSpec(**base, pixel_shuffle=True, drop_cls=True)
+    spec = core.ModelSpec("t", core.Architecture.DEC_ONLY, 56, 4, 1, encoder=enc)  # 4x4 grid -> 2x2
+    assert spec.encoder.out_width == 256
+    with pytest.raises(SpecError):  # 3x3 grid: odd
+        core.ModelSpec("t", core.Architecture.DEC_ONLY, 42, 4, 1, encoder=enc)
+    with pytest.raises(SpecError):  # tokens_per_tile inconsistent with the shuffle
+        core.ModelSpec("t", core.Architecture.DEC_ONLY, 56, 17, 1, encoder=enc)
+
+
+def test_internvit_random_init_layout():
+    import dataclasses
+
+    from paper_2502_00937_b200.weights import DEVICE_INIT_PARAMS, init_weights, param_count
+    spec = core.get_model_spec("internvl-26b")
+    assert param_count(spec) > DEVICE_INIT_PARAMS > param_count(core.get_model_spec("llama3.2-11b"))
+    small = dataclasses.replace(spec, encoder=dataclasses.replace(spec.encoder, layers=1, hidden=64, ffn=128,
+                                                                   heads=2))
+    W = init_weights(small, 0)
+    assert W["l0.ln1_b"] is None and W["l0.ln2_b"] is None and W["l0.qkv_b"] is None
+    assert W["l0.o_b"].shape == (64,) and W["patch_b"].shape == (64,)
+    for k in ("q_norm", "k_norm", "ls1", "ls2"):
+        assert W["l0." + k].shape == (64,)
+    assert W["pos"].shape == ((448 // 14) ** 2 + 1, 64) and W["cls"].shape == (64,)
