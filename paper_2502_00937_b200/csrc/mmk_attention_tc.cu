@@ -164,9 +164,11 @@ MMK_DEV void issue_s(uint32_t s_tm, uint32_t q_addr, uint32_t k_addr) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) umma_bf16_ss(s_tm, qd + 2 * k, kd + 2 * k, idesc_s, (b | k) > 0);
   }
+#ifndef MMK_ATTN_XP_NOSREM  // timing experiment only (make xp): S without its remainder k-step
   if (C::kRem)
     umma_bf16_ss(s_tm, umma_desc_sw32_kmajor(q_addr + C::kQMain), umma_desc_sw32_kmajor(k_addr + C::kKVMain),
                  idesc_s, 1u);
+#endif
 }
 
 // O_t (+)= P_t V for one KV tile: P_t from TMEM (bf16 pairs, 8 columns per 16 keys) as the A
