@@ -142,9 +142,11 @@ class CapturedEncode:
 
 class _GraphEntry:
     """One cached batch shape: the staged input buffer, the captured K0..K9 graph and its output.
-    ``run`` copies new pixels into the input buffer (per-image H2D from pinned tensors, or one H2D
-    from a page-locked staging copy) and replays; the returned tensors are fresh copies, so a
-    result never changes under its holder when the shape is encoded again."""
+    ``run`` copies new pixels in and replays; the returned tensors are fresh copies, so a result
+    never changes under its holder when the shape is encoded again.  Pinned-tensor inputs go
+    host-to-device on a copy stream into one of two landing buffers, so a call's H2D overlaps the
+    previous call's replay; the compute stream then moves them into the graph's input buffer with
+    one device copy.  Host arrays go through a page-locked staging copy."""
 
     def __init__(self, ex: "ImagePathExecutor", imgs: list):
         self.sizes = [int(im.shape[0]) * int(im.shape[1]) * 3 for im in imgs]
@@ -152,13 +154,32 @@ class _GraphEntry:
         self.host = None       # page-locked staging copy for host arrays (lazily)
         self.copied = None     # event after the last H2D out of ``host``
         self.cap = ex.capture(stage_images(imgs, ex.device))
+        self.copy_stream = None
+        self.landing, self.land_free, self.k = [], [None, None], 0
 
     def run(self, imgs: list) -> PackedBatch:
         src = self.cap.batch.src
         if all(isinstance(i, torch.Tensor) and i.device.type == "cpu" and i.is_pinned() and i.is_contiguous()
                for i in imgs):
-            for i, im in enumerate(imgs):
-                src[self.offs[i]:self.offs[i + 1]].copy_(im.view(-1), non_blocking=True)
+            if self.copy_stream is None:
+                self.copy_stream = torch.cuda.Stream(device=src.device)
+                self.landing = [torch.empty_like(src), torch.empty_like(src)]
+                for t in self.landing:  # freed (entry evicted) only once the copy stream is past them
+                    t.record_stream(self.copy_stream)
+            k, self.k = self.k, self.k ^ 1
+            land = self.landing[k]
+            compute = torch.cuda.current_stream(src.device)
+            with torch.cuda.stream(self.copy_stream):
+                if self.land_free[k] is not None:  # the device copy out of this buffer (two calls ago)
+                    self.copy_stream.wait_event(self.land_free[k])
+                for i, im in enumerate(imgs):
+                    land[self.offs[i]:self.offs[i + 1]].copy_(im.view(-1), non_blocking=True)
+                landed = torch.cuda.Event()
+                landed.record(self.copy_stream)
+            compute.wait_event(landed)
+            src.copy_(land)
+            self.land_free[k] = torch.cuda.Event()
+            self.land_free[k].record(compute)
         else:
             if self.host is None:
                 self.host = torch.empty(int(self.offs[-1]), dtype=torch.uint8, pin_memory=True)
