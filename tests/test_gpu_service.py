@@ -53,8 +53,10 @@ def test_executor_run_item_spans_match_direct_encode():
     assert torch.equal(out.embeds, direct.embeds)
 
 
-@pytest.mark.parametrize("model", ["llama3.2-11b", "llava-clip-l14-336"])
+@pytest.mark.parametrize("model", ["llama3.2-11b", "llava-clip-l14-336", "llava-ov-7b", "internvl-26b"])
 def test_projector_matches_torch(model):
+    """The LLM-side connector of each family (InternVL: LayerNorm(12800) -> MLP, its LayerNorm as
+    mmk_layernorm_bf16) against the same projection in fp32 torch."""
     from paper_2502_00937_b200 import core
     from paper_2502_00937_b200.connector import Projector
     spec = core.get_model_spec(model)
