@@ -118,6 +118,7 @@ preprocess_kernel(const uint8_t* __restrict__ src, const int64_t* __restrict__ s
   __shared__ int s_srow[kMaxSlots];                   // source row of each slot (ascending)
   __shared__ int s_rowoff[kMaxSlots * 3];             // per (chunk slot, plane): stage byte of pixel 0
   __shared__ int s_xa, s_rs, s_cap, s_nslot;
+  __shared__ __align__(8) uint64_t s_bar;  // staging: bulk-copy completion
   griddep_wait();  // PDL: inputs come from the preceding kernel
   griddep_launch_dependents();
 
@@ -157,6 +158,9 @@ preprocess_kernel(const uint8_t* __restrict__ src, const int64_t* __restrict__ s
   } else if (tid < 38) {
     const int c = tid - 32;
     s_nrm[c] = c < 3 ? scale3[c] : shift3[c - 3];
+  } else if (tid == 38) {
+    mbar_init(&s_bar, 1);
+    fence_barrier_init();
   }
   __syncthreads();
   const PrepImage m = meta;
@@ -333,29 +337,53 @@ preprocess_kernel(const uint8_t* __restrict__ src, const int64_t* __restrict__ s
     if (!direct) {
       if (sf > 0) __syncthreads();  // the previous chunk's rows are no longer read
       // stage: chunk slot s, plane c -> stage + (s*planes + c)*rs, copied from the 16-byte aligned
-      // address at or below the span start with asynchronous 16-byte copies, all in flight at
-      // once.  Reads stay inside [align16_down(image), image end): the aligned bytes before an
-      // image share its allocation (allocations are >= 256-byte aligned), and the vector holding
-      // the image's last byte is zero-filled past it.  A warp per (slot, plane), lanes over the
-      // row's vectors.
+      // address at or below the span start.  Warp 0 issues a bulk copy per row, a lane per row (the
+      // TMA engine moves the bytes; completion counted on s_bar) for the whole 16-byte vectors inside
+      // the image; the vector holding the image's last byte and any past it go by cp.async with zero
+      // fill.  Reads stay inside [align16_down(image), image end): the aligned bytes before an
+      // image share its allocation (allocations are >= 256-byte aligned).
       const uint8_t* img_end = img + (CHW ? 3 * plane : row_bytes * m.h);
-      const int nvec = rs >> 4;
-      for (int r = wid; r < nsl * planes; r += nwarps) {
-        const int s = CHW ? r / 3 : r, c = CHW ? r - 3 * s : 0;
-        const uint8_t* span = img + c * plane + static_cast<int64_t>(s_srow[sf + s]) * row_bytes + bpp * xa;
-        const uint8_t* gA = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(span) & ~uintptr_t(15));
-        const uint32_t dst = stage_s + r * rs;
-        if (lane == 0) s_rowoff[r] = r * rs + static_cast<int>(span - gA) - bpp * xa;
-        for (int v = lane; v < nvec; v += 32) {
-          const uint8_t* gv = gA + 16 * v;
-          const int64_t left = img_end - gv;
-          const uint32_t nb = left >= 16 ? 16u : (left > 0 ? static_cast<uint32_t>(left) : 0u);
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + 16 * v), "l"(nb ? gv : img),
-                       "r"(nb)
-                       : "memory");
+      if (wid == 0) {  // warp 0: lane l owns rows l, l + 32, ...
+        const int nrow = nsl * planes;
+        auto row_src = [&](int r, const uint8_t*& span, const uint8_t*& gA) {
+          const int s = CHW ? r / 3 : r, c = CHW ? r - 3 * s : 0;
+          span = img + c * plane + static_cast<int64_t>(s_srow[sf + s]) * row_bytes + bpp * xa;
+          gA = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(span) & ~uintptr_t(15));
+        };
+        auto whole = [&](const uint8_t* gA) {  // bytes of whole vectors inside the image
+          const int64_t left = img_end - gA;
+          return left >= rs ? static_cast<uint32_t>(rs) : static_cast<uint32_t>(left > 0 ? left & ~int64_t(15) : 0);
+        };
+        uint32_t tx = 0;
+        for (int r = lane; r < nrow; r += 32) {
+          const uint8_t *span, *gA;
+          row_src(r, span, gA);
+          tx += whole(gA);
+          s_rowoff[r] = r * rs + static_cast<int>(span - gA) - bpp * xa;
         }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, o);
+        if (lane == 0) mbar_arrive_expect_tx(&s_bar, tx);
+        __syncwarp();
+        const uint32_t bar = smem_u32(&s_bar);
+        for (int r = lane; r < nrow; r += 32) {
+          const uint8_t *span, *gA;
+          row_src(r, span, gA);
+          const uint32_t full = whole(gA), dst = stage_s + r * rs;
+          if (full)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(dst), "l"(gA), "r"(full), "r"(bar) : "memory");
+          for (uint32_t v = full; v < static_cast<uint32_t>(rs); v += 16) {
+            const int64_t left = img_end - (gA + v);
+            const uint32_t nb = left >= 16 ? 16u : (left > 0 ? static_cast<uint32_t>(left) : 0u);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + v), "l"(nb ? gA + v : img),
+                         "r"(nb)
+                         : "memory");
+          }
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
       }
-      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+      mbar_wait(&s_bar, static_cast<uint32_t>(sf / chunk) & 1u);
       __syncthreads();
     }
     if (active) {
