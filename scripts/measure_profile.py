@@ -5,7 +5,7 @@
 
 Writes profiles/measured_<model>.json (MeasuredProfile) and profiles/measured_<model>.reference.json
 (the reference's profile schema, profiles.py:268-326, LLM-side fields from
-tests/golden/profile_llama.json, image-stage fields measured), which the reference's own
+tests/golden/profile_<model>.json, image-stage fields measured), which the reference's own
 LatencyProfile.from_dict loads (tests/test_profiles.py).  ``--scale`` takes bench.py JSON lines
 at N GPUs to fill dp_efficiency (throughput / (N x one-GPU throughput)).
 """
@@ -22,13 +22,20 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--model", default="llama3.2-11b")
     ap.add_argument("--scale", nargs="*", default=[])
+    ap.add_argument("--export-only", action="store_true",
+                    help="no measurement: re-export the committed profiles/measured_<model>.json (CPU)")
     args = ap.parse_args()
-    import torch
     from paper_2502_00937_b200 import core
-    from paper_2502_00937_b200.executor import ImagePathExecutor
-    from paper_2502_00937_b200.profiles import measure_profile
+    from paper_2502_00937_b200.profiles import MeasuredProfile
     spec = core.get_model_spec(args.model)
-    prof = measure_profile(ImagePathExecutor(spec, seed=0))
+    if args.export_only:
+        path = os.path.join(ROOT, "profiles", f"measured_{spec.name}.json")
+        prof = MeasuredProfile.from_dict(json.loads(open(path).read()), spec)
+    else:
+        import torch  # noqa: F401
+        from paper_2502_00937_b200.executor import ImagePathExecutor
+        from paper_2502_00937_b200.profiles import measure_profile
+        prof = measure_profile(ImagePathExecutor(spec, seed=0))
     lines = [json.loads(open(p).read().strip().splitlines()[-1]) for p in args.scale]
     one = [d["value"] for d in lines if d.get("n_gpus") == 1]
     if one:
@@ -37,12 +44,17 @@ def main():
                 prof.dp_efficiency[int(d["n_gpus"])] = round(d["value"] / (d["n_gpus"] * one[0]), 4)
     out = os.path.join(ROOT, "profiles", f"measured_{spec.name}.json")
     prof.save(out)
-    base = json.loads(open(os.path.join(ROOT, "tests", "golden", "profile_llama.json")).read())
+    # LLM-side fields from the reference's own calibrated profile of the preset (tests/golden,
+    # made by running the reference: make_golden.py)
+    gold = os.path.join(ROOT, "tests", "golden", f"profile_{spec.name}.json")
+    if not os.path.exists(gold):
+        gold = os.path.join(ROOT, "tests", "golden", "profile_llama.json")
+    base = json.loads(open(gold).read())
     if base.get("model") == spec.name:
         ref = prof.to_reference_profile(base)
         open(os.path.join(ROOT, "profiles", f"measured_{spec.name}.reference.json"), "w").write(
             json.dumps(ref, indent=2) + "\n")
-    print(json.dumps({"model": spec.name, "device": torch.cuda.get_device_name(), **prof.to_dict()}))
+    print(json.dumps({"model": spec.name, **prof.to_dict()}))
 
 
 if __name__ == "__main__":

@@ -145,11 +145,16 @@ def policies():
 
 
 def profile():
-    """The reference's own calibrated profile (profiles.py:400-470) — base for the export test."""
+    """The reference's own calibrated profiles (profiles.py:400-470, default_profile :549) — the
+    base (LLM-side fields) of the B200-measured profile exports, one per preset."""
     from lmmsim import profiles as rprof
     spec = rcore.get_model_spec("llama3.2-11b")
     prof = rprof.calibrate(rprof.load_calibration_targets(spec.name), spec)
     (OUT / "profile_llama.json").write_text(json.dumps(prof.to_dict(), indent=1))
+    for name in ("internvl-26b", "llava-ov-7b"):
+        spec = rcore.get_model_spec(name)
+        prof = rprof.default_profile(spec)
+        (OUT / f"profile_{name}.json").write_text(json.dumps(prof.to_dict(), indent=1))
 
 
 if __name__ == "__main__":

@@ -82,23 +82,30 @@ def test_batch_priced_from_its_tile_histogram():
     assert q.tile_costs == p.tile_costs and q.dp_efficiency == p.dp_efficiency
 
 
-MEASURED = Path(__file__).resolve().parent.parent / "profiles" / "measured_llama3.2-11b.reference.json"
+PROFILES = Path(__file__).resolve().parent.parent / "profiles"
 
 
-@pytest.mark.skipif(not MEASURED.exists(), reason="no B200-measured profile committed")
-def test_committed_b200_profile_loads_in_the_reference():
+@pytest.mark.parametrize("model", ["llama3.2-11b", "internvl-26b", "llava-ov-7b"])
+def test_committed_b200_profile_loads_in_the_reference(model):
     """The B200-measured profile (scripts/measure_profile.py on a B200) in the reference schema,
-    loaded by the reference's own LatencyProfile.from_dict (profiles.py:299-326)."""
-    ref = json.loads(MEASURED.read_text())
-    mp = MeasuredProfile.from_dict(json.loads((MEASURED.parent / "measured_llama3.2-11b.json").read_text()), LLAMA)
-    assert len(mp.encode_points) >= 3 and set(mp.tile_costs) >= {1, 2, 4}
-    assert mp.tile_costs[4] > 2 * mp.tile_costs[2] > 0  # super-linear in tiles
+    loaded by the reference's own LatencyProfile.from_dict (profiles.py:299-326); LLM-side fields
+    from the reference's calibrated profile of the same preset (tests/golden/profile_<model>.json)."""
+    measured = PROFILES / f"measured_{model}.reference.json"
+    if not measured.exists():
+        pytest.skip("no B200-measured profile committed")
+    spec = core.get_model_spec(model)
+    ref = json.loads(measured.read_text())
+    assert ref["model"] == model
+    mp = MeasuredProfile.from_dict(json.loads((PROFILES / f"measured_{model}.json").read_text()), spec)
+    assert len(mp.encode_points) >= 3 and len(mp.tile_costs) >= 3
+    if model == "llama3.2-11b":
+        assert mp.tile_costs[4] > 2 * mp.tile_costs[2] > 0  # super-linear in tiles (cross-tile attention)
     if not Path("/root/reference/pkg/src").exists():
         pytest.skip("reference not mounted")
     sys.path.insert(0, "/root/reference/pkg/src")
     from lmmsim import core as rcore
     from lmmsim import profiles as rprofiles
-    rp = rprofiles.LatencyProfile.from_dict(ref, rcore.get_model_spec("llama3.2-11b"))
+    rp = rprofiles.LatencyProfile.from_dict(ref, rcore.get_model_spec(model))
     t, ms = mp.encode_points[-1]
     assert rp.encode_latency(t, 1) == pytest.approx(ms, rel=1e-6)
     for tp in (2, 4, 8):
