@@ -43,18 +43,21 @@ def _worker(rank, world, port, q):
         got = {src: buf.clone() for src, buf in h.received.items()}
         ok = True
         for src, buf in got.items():
-            expect = torch.cat([torch.full((tiles[i] * spec.tokens_per_tile, width), float(i)) for i in shards[src]])
+            expect = torch.cat([torch.full((tiles[i] * spec.tokens_per_tile, width), float(i)) for i in shards[src]]
+                               + [torch.zeros(0, width)])
             ok &= torch.equal(buf, expect + 2)
         q.put((ok, [sorted(s) for s in shards]))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_partition_and_handoff_gloo_world2():
+@pytest.mark.parametrize("world", [2, 8])
+def test_partition_and_handoff_gloo(world):
+    """World 8 with 6 images: two ranks hold empty shards (zero-row sends and receives)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     ok, shards = q.get(timeout=120)
