@@ -24,13 +24,24 @@ def main():
     ap.add_argument("--scale", nargs="*", default=[])
     ap.add_argument("--export-only", action="store_true",
                     help="no measurement: re-export the committed profiles/measured_<model>.json (CPU)")
+    ap.add_argument("--from-model", default=None,
+                    help="with --export-only: take the measurement of a preset with the same image path "
+                         "(encoder block and tiling), e.g. llama3.2-11b for llama3.2-90b")
     args = ap.parse_args()
     from paper_2502_00937_b200 import core
     from paper_2502_00937_b200.profiles import MeasuredProfile
     spec = core.get_model_spec(args.model)
     if args.export_only:
-        path = os.path.join(ROOT, "profiles", f"measured_{spec.name}.json")
-        prof = MeasuredProfile.from_dict(json.loads(open(path).read()), spec)
+        src = core.get_model_spec(args.from_model or args.model)
+        same = (src.encoder == spec.encoder and src.tile_edge_px == spec.tile_edge_px
+                and src.max_tiles_per_image == spec.max_tiles_per_image and src.thumbnail_tile == spec.thumbnail_tile)
+        if not same:
+            raise SystemExit(f"{src.name} and {spec.name} do not share the image path")
+        d = json.loads(open(os.path.join(ROOT, "profiles", f"measured_{src.name}.json")).read())
+        if src.name != spec.name:
+            d["model"] = spec.name
+            d.setdefault("meta", {})["measured_as"] = src.name
+        prof = MeasuredProfile.from_dict(d, spec)
     else:
         import torch  # noqa: F401
         from paper_2502_00937_b200.executor import ImagePathExecutor

@@ -151,7 +151,7 @@ def profile():
     spec = rcore.get_model_spec("llama3.2-11b")
     prof = rprof.calibrate(rprof.load_calibration_targets(spec.name), spec)
     (OUT / "profile_llama.json").write_text(json.dumps(prof.to_dict(), indent=1))
-    for name in ("internvl-26b", "llava-ov-7b"):
+    for name in ("internvl-26b", "llava-ov-7b", "llama3.2-90b", "llava-ov-72b", "nvlm-d-72b"):
         spec = rcore.get_model_spec(name)
         prof = rprof.default_profile(spec)
         (OUT / f"profile_{name}.json").write_text(json.dumps(prof.to_dict(), indent=1))

@@ -85,7 +85,8 @@ def test_batch_priced_from_its_tile_histogram():
 PROFILES = Path(__file__).resolve().parent.parent / "profiles"
 
 
-@pytest.mark.parametrize("model", ["llama3.2-11b", "internvl-26b", "llava-ov-7b"])
+@pytest.mark.parametrize("model", ["llama3.2-11b", "llama3.2-90b", "internvl-26b", "nvlm-d-72b", "llava-ov-7b",
+                                   "llava-ov-72b"])
 def test_committed_b200_profile_loads_in_the_reference(model):
     """The B200-measured profile (scripts/measure_profile.py on a B200) in the reference schema,
     loaded by the reference's own LatencyProfile.from_dict (profiles.py:299-326); LLM-side fields
@@ -98,7 +99,7 @@ def test_committed_b200_profile_loads_in_the_reference(model):
     assert ref["model"] == model
     mp = MeasuredProfile.from_dict(json.loads((PROFILES / f"measured_{model}.json").read_text()), spec)
     assert len(mp.encode_points) >= 3 and len(mp.tile_costs) >= 3
-    if model == "llama3.2-11b":
+    if model.startswith("llama3.2"):
         assert mp.tile_costs[4] > 2 * mp.tile_costs[2] > 0  # super-linear in tiles (cross-tile attention)
     if not Path("/root/reference/pkg/src").exists():
         pytest.skip("reference not mounted")
