@@ -127,7 +127,7 @@ def main():
         dev = torch.device("cuda", local)
         if args.handoff == "peer":
             enc = spec.encoder
-            P1 = spec.seq_per_tile
+            P1 = spec.tokens_per_tile  # emitted rows per tile (InternVL: 256 of its 1025 encoder tokens)
             width = enc.out_width
             chan = PeerShardChannel(rank, world, dev, torch.bfloat16, slot_rows=args.slot_images * spec.max_tiles_per_image * P1,
                                     width=width, **kw)
