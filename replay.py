@@ -143,7 +143,8 @@ def main():
                           "images_per_request": IMAGES_PER_REQUEST, "requests": len(reqs), "images": n_img},
                 "batcher": {"router": "least_pending", "scheduler": args.scheduler, "max_batch_encode": args.max_batch,
                             "router_cost_model": cost_src},
-                "connector": "mllama multi_modal_projector on rank 0" if args.connector else None,
+                "connector": (f"{spec.name} multi_modal_projector ({spec.encoder.out_width} -> 4096) on rank 0"
+                              if args.connector else None),
                 "handoff": (args.handoff if world > 1 else None),
                 "handoff_shards": (dict(chan.counts) if chan is not None else None),
                 "model": spec.name}
