@@ -33,3 +33,22 @@ def test_replay_handoff_bit_exact(handoff, port, model, slot_images):
         assert line["handoff_shards"]["peer"] > 0
     if slot_images == 1:
         assert line["handoff_shards"]["nccl"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("scaling,port", [("weak", 29541), ("strong", 29542)])
+def test_bench_two_gpus_json_line(scaling, port):
+    """bench.py under torchrun at N=2 (the driver's scaling launch): one JSON line from rank 0 with
+    n_gpus 2, the whole-job value, the partition and the NVLink handoff inside the timed region."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--scaling", scaling, "--model", "vit-b16-224"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == scaling and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert d["config"]["parallelism"].startswith("dp2") and "cpu_baseline" not in d
+    assert d["config"]["images_per_step"] == (16 if scaling == "weak" else 32)
