@@ -501,6 +501,16 @@ def test_abi_status_codes_map_to_reference_exceptions(mk):
     out = torch.empty(8 * 64 * 2 + 8, dtype=torch.bfloat16, device="cuda")[1:1 + 8 * 128].view(8, 128)
     with pytest.raises(SpecError, match="aligned"):
         ops.pack_mllama(fin, inter[:1], out=out, peer=True)                  # 2-byte offset
+    # InternViT entry points
+    src = torch.randn(2 * 10, 64, device="cuda")
+    with pytest.raises(SpecError, match="pack_pixel_shuffle"):
+        ops.pack_pixel_shuffle(src, 2, 3, 10, 1)                               # odd 3x3 grid
+    q = torch.randn(4, 3 * 100, device="cuda").bfloat16()
+    w = torch.ones(100, device="cuda")
+    with pytest.raises(SpecError, match="qk_rmsnorm"):
+        ops.qk_rmsnorm(q, 100, w, w, 1e-6)                                    # d % 8 != 0
+    with pytest.raises(SpecError, match="ln_stats_finalize"):
+        ops.ln_stats_finalize(torch.zeros(4, 2, 2, device="cuda"), 4, 48, 1e-5)  # d % 32 != 0
     # the context stays usable after every rejected call
     torch.cuda.synchronize()
     assert torch.equal(ops.pack_mllama(fin, inter[:1], peer=True), ops.pack_mllama(fin, inter[:1]))
